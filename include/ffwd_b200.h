@@ -1,0 +1,131 @@
+/*
+ * ffwd_b200.h — C-ABI boundary of the B200-native FastForward prefill-FFN hot path.
+ *
+ * The reference (arXiv 2602.00397, /root/reference/pkg/src/sparseprefill) has no
+ * FFI: the path is plain Python calls from engine.py:284-300.  These entry points
+ * are what a binding of that path needs; each one names the
+ * reference function(s) it replaces.  The Python package
+ * paper_2602_00397_b200 binds them with ctypes.
+ *
+ * Conventions
+ *   - every pointer argument is a DEVICE pointer unless stated otherwise;
+ *     buffers are caller owned and never retained after return;
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream); all work is
+ *     stream ordered, nothing synchronises the host;
+ *   - bf16 buffers are passed as `const void*` (IEEE bfloat16, row-major);
+ *   - return value: FFWD_OK or an error code; ffwd_last_error() gives the
+ *     message (thread local).  FFWD_ERR_VALIDATION mirrors the reference's
+ *     ValidationError (errors.py:9) and is raised before any launch.
+ *
+ * Weight layouts (built once per layer by paper_2602_00397_b200.layer.pack_layer):
+ *   wgu_t  bf16 [(2*f_local + rc_up_rows) x d]  rows: gate^T | up^T | Wc1^T | 0-pad
+ *          (model.py:79 w_gate/w_up (d, f) transposed to neuron-major;
+ *           compensator.py:25-39 w1 (d, r') transposed), rc_up_rows = roundup(rc_local, 256)
+ *   wd     bf16 [(f_local + rc_dn_rows) x d]    rows: W_down | Wc2 | 0-pad,
+ *          rc_dn_rows = roundup(rc_local, 64)
+ *   Under tensor parallelism rank s holds neurons {j : j % tp_size == s} (local
+ *   row j / tp_size) and compensator columns [s*rc/tp, (s+1)*rc/tp).
+ */
+#ifndef FFWD_B200_H
+#define FFWD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define FFWD_API __attribute__((visibility("default")))
+#else
+#define FFWD_API
+#endif
+
+#define FFWD_ABI_VERSION 1
+
+#define FFWD_OK 0
+#define FFWD_ERR_VALIDATION 1  /* bad shape / k / index set  -> ValidationError */
+#define FFWD_ERR_CUDA 2        /* CUDA runtime or launch error -> RuntimeError  */
+#define FFWD_ERR_UNSUPPORTED 3 /* no sm_100 device / shape outside kernel limits */
+
+FFWD_API int ffwd_abi_version(void);
+FFWD_API const char* ffwd_last_error(void);
+
+/* 0 when `device` is an sm_100 (B200-class) GPU; FFWD_ERR_UNSUPPORTED otherwise. */
+FFWD_API int ffwd_device_check(int device);
+
+/* Tuning knobs of the gather-GEMM rasterisation (blocks per L2 group). */
+FFWD_API int ffwd_set_raster(int up_group, int down_group);
+
+/*
+ * Predictor scores for blocks [blk_begin, blk_begin + blk_count) of x.
+ * Replaces predictor.py:68-81 predictor_forward (called per block at engine.py:286):
+ *   scores[i, :] = relu(f32(pool(x_blk) . w1)) . w2 with f64 accumulation,
+ *   bit-identical to the reference.
+ * x: [T x d] f32 (x_is_f32 = 1) or bf16; query f32 [d]; w1 f32 [d x r];
+ * w2 f32 [r x f]; scores f32 [blk_count x f].
+ */
+FFWD_API size_t ffwd_predictor_workspace_bytes(int blk_count, int d, int r);
+FFWD_API int ffwd_predictor_forward(const void* x, int x_is_f32, int T, int d, int blk_begin,
+                           int blk_count, const float* query, const float* w1, const float* w2,
+                           int r, int f, float* scores, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
+/*
+ * Per-row top-k.  Replaces kernels.py:139-149 topk_indices / sparse.py:49-55 build_mask:
+ * ties keep the lower index, -0 == +0, NaN after every number, result ascending.
+ * idx_global [n_rows x ld_global] (nullable) receives global neuron ids; with
+ * tp_size > 1, idx_local [n_rows x ld_local] (nullable) receives the rank-local
+ * ids j / tp_size of the selected neurons with j % tp_size == tp_rank and
+ * counts [n_rows] (nullable) their number.
+ */
+FFWD_API int ffwd_topk(const float* scores, int n_rows, int f, int k, int tp_rank, int tp_size,
+              int32_t* idx_global, int ld_global, int32_t* idx_local, int ld_local,
+              int32_t* counts, void* stream);
+
+/* predictor_forward + build_mask fused into one stream-ordered call. */
+FFWD_API int ffwd_predict_topk(const void* x, int x_is_f32, int T, int d, int blk_begin, int blk_count,
+                      const float* query, const float* w1, const float* w2, int r, int f, int k,
+                      int tp_rank, int tp_size, int32_t* idx_global, int ld_global,
+                      int32_t* idx_local, int ld_local, int32_t* counts, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
+/*
+ * Sparse SwiGLU FFN (+ optional compensator) over every 128-token block of x.
+ * Replaces sparse.py:66-91 select_subweights + sparse_ffn_forward and, with
+ * has_comp, compensator.py:52-66 compensator_forward + apply_compensation; with
+ * idx == NULL it is engine.py:127-131 dense_ffn.
+ * idx: [n_idx_rows x ld_idx] int32 ascending rank-local neuron ids; one row per
+ * block when idx_per_block, else row 0 is shared by all blocks; counts
+ * (nullable) gives per-row k, else k for every row.
+ * y: f32 [T x d] (partial sum of this rank under tensor parallelism).
+ */
+FFWD_API size_t ffwd_sparse_ffn_workspace_bytes(int T, int d, int f_local, int rc_local, int k);
+FFWD_API int ffwd_sparse_ffn(const void* x_bf16, int T, int d, const void* wgu_t, const void* wd,
+                    int f_local, int rc_local, const int32_t* idx, int idx_per_block, int ld_idx,
+                    const int32_t* counts, int k, int has_comp, float* y, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/*
+ * One layer of the FFN branch of the block-wise prefill, all blocks at once.
+ * Replaces the engine.py:254-310 FFN branch (mode "predicted") for one layer:
+ * dense first/last block when dense_first_last (engine.py:258-262), dense when
+ * k >= f_global (engine.py:268), otherwise predictor -> top-k -> sparse FFN ->
+ * compensation (has_comp).  The residual add (engine.py:308) stays with the
+ * caller.  idx_global (nullable, [n_sparse x ld_idx_global]) receives the
+ * selected global neuron ids of every predicted block.
+ */
+FFWD_API size_t ffwd_layer_workspace_bytes(int T, int d, int f_global, int f_local, int rc_local, int r,
+                                  int k, int dense_first_last, int tp_size);
+FFWD_API int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t, const void* wd,
+                   int f_local, int rc_local, const float* query, const float* w1,
+                   const float* w2, int r, int f_global, int k, int dense_first_last,
+                   int has_comp, int tp_rank, int tp_size, float* y, int32_t* idx_global,
+                   int ld_idx_global, void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FFWD_B200_H */

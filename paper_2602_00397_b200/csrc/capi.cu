@@ -1,0 +1,366 @@
+// extern "C" boundary (include/ffwd_b200.h): validation with the reference's
+// error semantics, workspace carving, and the per-layer launch sequence
+//   pool -> W1 -> W2 -> top-k -> plan -> up-proj (K2) -> down-proj (K3).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/ffwd_b200.h"
+#include "ffwd_internal.h"
+
+using namespace ffwd;
+
+namespace {
+
+thread_local std::string g_err;
+int g_up_group = 32;
+int g_down_group = 8;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(FFWD_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+#define FFWD_CUDA(call, where)                    \
+  do {                                            \
+    cudaError_t _e = (call);                      \
+    if (_e != cudaSuccess) return cuda_fail(_e, where); \
+  } while (0)
+
+int rup(int v, int m) { return (v + m - 1) / m * m; }
+size_t al(size_t v) { return (v + 255) & ~size_t(255); }
+
+int num_sms() {
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+int bn_for(int d) { return d % 256 == 0 ? 256 : (d % 128 == 0 ? 128 : 64); }
+
+// Workspace carve-out helper: sequential 256 B aligned sub-allocations.
+struct Carve {
+  char* base;
+  size_t off = 0;
+  explicit Carve(void* p) : base(static_cast<char*>(p)) {}
+  template <typename T>
+  T* take(size_t n) {
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += al(n * sizeof(T));
+    return p;
+  }
+};
+
+struct Pred {
+  float* pooled;
+  float* hidden;
+  float* scores;
+};
+
+Pred carve_pred(Carve& c, int nb, int d, int r, int f) {
+  Pred p;
+  p.pooled = c.take<float>(static_cast<size_t>(nb) * d);
+  p.hidden = c.take<float>(static_cast<size_t>(nb) * r);
+  p.scores = c.take<float>(static_cast<size_t>(nb) * f);
+  return p;
+}
+
+struct Ffn {
+  int32_t* idx_local;
+  int32_t* counts;
+  BlockMeta* meta;
+  Tile* up;
+  Tile* down;
+  PlanCounts* pc;
+  __nv_bfloat16* h;
+  int up_cap, down_cap, hcols, ld_local;
+};
+
+// kmax: largest per-block neuron count of a predicted block (rank local)
+Ffn carve_ffn(Carve& c, int T, int d, int f_local, int rc_local, int kmax, int n_sparse,
+              int ld_local) {
+  Ffn w;
+  const int n_blk = (T + kBlockTokens - 1) / kBlockTokens;
+  const int rc64 = rup(rc_local, 64);
+  const int tiles_dense = (f_local + 127) / 128;
+  const int tiles_sparse = (kmax + 127) / 128 + (rc64 + 255) / 256;
+  w.up_cap = n_blk * (tiles_dense > tiles_sparse ? tiles_dense : tiles_sparse);
+  w.down_cap = n_blk * (d / bn_for(d));
+  w.hcols = rup(rup(f_local, 64) > rup(kmax, 64) + rc64 ? rup(f_local, 64) : rup(kmax, 64) + rc64,
+                64);
+  w.ld_local = ld_local;
+  w.idx_local = c.take<int32_t>(static_cast<size_t>(n_sparse > 0 ? n_sparse : 1) * ld_local);
+  w.counts = c.take<int32_t>(n_sparse > 0 ? n_sparse : 1);
+  w.meta = c.take<BlockMeta>(n_blk);
+  w.up = c.take<Tile>(w.up_cap);
+  w.down = c.take<Tile>(w.down_cap);
+  w.pc = c.take<PlanCounts>(1);
+  w.h = c.take<__nv_bfloat16>(static_cast<size_t>(n_blk) * kBlockTokens * w.hcols);
+  return w;
+}
+
+int check_common(int T, int d, int f, int k) {
+  if (T < 1) return fail(FFWD_ERR_VALIDATION, "token count must be >= 1, got %d", T);
+  if (d < 1 || f < 1) return fail(FFWD_ERR_VALIDATION, "bad dims d=%d f=%d", d, f);
+  if (k < 1 || k > f) return fail(FFWD_ERR_VALIDATION, "k=%d out of range [1, %d]", k, f);
+  return FFWD_OK;
+}
+
+int run_ffn(const void* x, int T, int d, const void* wgu_t, const void* wd, int f_local,
+            int rc_local, const Ffn& w, const int32_t* idx, int ld_idx, int sparse_begin,
+            int sparse_count, const int32_t* counts, int k_shared, int idx_shared, int has_comp,
+            float* y, cudaStream_t s) {
+  const int n_blk = (T + kBlockTokens - 1) / kBlockTokens;
+  PlanArgs pa{};
+  pa.T = T;
+  pa.d = d;
+  pa.f_local = f_local;
+  pa.rc_local = has_comp ? rc_local : 0;
+  pa.n_blk = n_blk;
+  pa.sparse_begin = sparse_begin;
+  pa.sparse_count = sparse_count;
+  pa.k_shared = k_shared;
+  pa.counts = counts;
+  pa.idx_shared = idx_shared;
+  pa.has_comp = has_comp;
+  pa.up_group = g_up_group;
+  pa.down_group = g_down_group;
+  pa.bn_down = bn_for(d);
+  pa.hcols_alloc = w.hcols;
+  FFWD_CUDA(launch_plan(pa, w.meta, w.up, w.up_cap, w.down, w.down_cap, w.pc, s), "plan");
+  GemmArgs ga{};
+  ga.x = x;
+  ga.wgu_t = wgu_t;
+  ga.wgu_rows = 2 * f_local + rup(rc_local, 256);
+  ga.wd = wd;
+  ga.wd_rows = f_local + rup(rc_local, 64);
+  ga.h = w.h;
+  ga.hcols = w.hcols;
+  ga.y = y;
+  ga.T = T;
+  ga.d = d;
+  ga.f_local = f_local;
+  ga.n_blk = n_blk;
+  ga.idx = idx;
+  ga.ld_idx = ld_idx;
+  ga.meta = w.meta;
+  ga.up_tiles = w.up;
+  ga.up_cap = w.up_cap;
+  ga.down_tiles = w.down;
+  ga.down_cap = w.down_cap;
+  ga.counts = w.pc;
+  ga.num_sms = num_sms();
+  ga.bn_down = bn_for(d);
+  FFWD_CUDA(launch_up_proj(ga, s), "up_proj");
+  FFWD_CUDA(launch_down_proj(ga, s), "down_proj");
+  return FFWD_OK;
+}
+
+int check_gemm_shapes(int d, int f_local) {
+  if (d % 64 != 0)
+    return fail(FFWD_ERR_UNSUPPORTED, "d_model=%d: the sm_100a path needs d_model %% 64 == 0", d);
+  if (f_local < 1) return fail(FFWD_ERR_VALIDATION, "f_local must be >= 1");
+  return FFWD_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ffwd_abi_version(void) { return FFWD_ABI_VERSION; }
+
+const char* ffwd_last_error(void) { return g_err.c_str(); }
+
+int ffwd_device_check(int device) {
+  cudaDeviceProp p;
+  cudaError_t e = cudaGetDeviceProperties(&p, device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+  if (p.major != 10 || p.minor != 0)
+    return fail(FFWD_ERR_UNSUPPORTED, "device %d is sm_%d%d; kernels are built for sm_100a",
+                device, p.major, p.minor);
+  return FFWD_OK;
+}
+
+int ffwd_set_raster(int up_group, int down_group) {
+  if (up_group < 1 || down_group < 1)
+    return fail(FFWD_ERR_VALIDATION, "raster groups must be >= 1");
+  g_up_group = up_group;
+  g_down_group = down_group;
+  return FFWD_OK;
+}
+
+size_t ffwd_predictor_workspace_bytes(int blk_count, int d, int r) {
+  Carve c(nullptr);
+  carve_pred(c, blk_count, d, r, 0);
+  return c.off;
+}
+
+int ffwd_predictor_forward(const void* x, int x_is_f32, int T, int d, int blk_begin,
+                           int blk_count, const float* query, const float* w1, const float* w2,
+                           int r, int f, float* scores, void* workspace, size_t workspace_bytes,
+                           void* stream) {
+  g_err.clear();
+  if (T < 1 || d < 1 || r < 1 || f < 1)
+    return fail(FFWD_ERR_VALIDATION, "predictor dims T=%d d=%d r=%d f=%d", T, d, r, f);
+  if (d % 8 != 0)
+    return fail(FFWD_ERR_UNSUPPORTED, "predictor needs d_model %% 8 == 0, got %d", d);
+  const int n_blk = (T + kBlockTokens - 1) / kBlockTokens;
+  if (blk_begin < 0 || blk_count < 0 || blk_begin + blk_count > n_blk)
+    return fail(FFWD_ERR_VALIDATION, "block range [%d, %d) outside [0, %d)", blk_begin,
+                blk_begin + blk_count, n_blk);
+  if (workspace_bytes < ffwd_predictor_workspace_bytes(blk_count, d, r))
+    return fail(FFWD_ERR_VALIDATION, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carve c(workspace);
+  Pred p = carve_pred(c, blk_count, d, r, 0);
+  const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));
+  FFWD_CUDA(launch_pool(x, x_is_f32 != 0, T, d, blk_begin, blk_count, query, sqrt_d, p.pooled, s),
+            "pool");
+  FFWD_CUDA(launch_gemm_f64acc(p.pooled, w1, p.hidden, blk_count, d, r, true, s), "w1");
+  FFWD_CUDA(launch_gemm_f64acc(p.hidden, w2, scores, blk_count, r, f, false, s), "w2");
+  return FFWD_OK;
+}
+
+int ffwd_topk(const float* scores, int n_rows, int f, int k, int tp_rank, int tp_size,
+              int32_t* idx_global, int ld_global, int32_t* idx_local, int ld_local,
+              int32_t* counts, void* stream) {
+  g_err.clear();
+  if (n_rows < 0 || f < 1) return fail(FFWD_ERR_VALIDATION, "bad top-k shape");
+  if (k < 1 || k > f) return fail(FFWD_ERR_VALIDATION, "k=%d out of range [1, %d]", k, f);
+  if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size)
+    return fail(FFWD_ERR_VALIDATION, "bad tensor-parallel rank %d of %d", tp_rank, tp_size);
+  if (idx_global && ld_global < k) return fail(FFWD_ERR_VALIDATION, "ld_global < k");
+  FFWD_CUDA(launch_topk(scores, n_rows, f, k, tp_rank, tp_size, idx_global, ld_global, idx_local,
+                        ld_local, counts, static_cast<cudaStream_t>(stream)),
+            "topk");
+  return FFWD_OK;
+}
+
+int ffwd_predict_topk(const void* x, int x_is_f32, int T, int d, int blk_begin, int blk_count,
+                      const float* query, const float* w1, const float* w2, int r, int f, int k,
+                      int tp_rank, int tp_size, int32_t* idx_global, int ld_global,
+                      int32_t* idx_local, int ld_local, int32_t* counts, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  const size_t need = ffwd_predictor_workspace_bytes(blk_count, d, r) +
+                      al(static_cast<size_t>(blk_count) * f * sizeof(float));
+  if (workspace_bytes < need) return fail(FFWD_ERR_VALIDATION, "workspace too small");
+  float* scores = reinterpret_cast<float*>(static_cast<char*>(workspace) +
+                                           ffwd_predictor_workspace_bytes(blk_count, d, r));
+  int rc = ffwd_predictor_forward(x, x_is_f32, T, d, blk_begin, blk_count, query, w1, w2, r, f,
+                                  scores, workspace, workspace_bytes, stream);
+  if (rc != FFWD_OK) return rc;
+  return ffwd_topk(scores, blk_count, f, k, tp_rank, tp_size, idx_global, ld_global, idx_local,
+                   ld_local, counts, stream);
+}
+
+size_t ffwd_sparse_ffn_workspace_bytes(int T, int d, int f_local, int rc_local, int k) {
+  Carve c(nullptr);
+  carve_ffn(c, T, d, f_local, rc_local, k, 0, 4);
+  return c.off;
+}
+
+int ffwd_sparse_ffn(const void* x_bf16, int T, int d, const void* wgu_t, const void* wd,
+                    int f_local, int rc_local, const int32_t* idx, int idx_per_block, int ld_idx,
+                    const int32_t* counts, int k, int has_comp, float* y, void* workspace,
+                    size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  int rc = check_common(T, d, f_local, k);
+  if (rc) return rc;
+  if ((rc = check_gemm_shapes(d, f_local))) return rc;
+  if (has_comp && rc_local < 1) return fail(FFWD_ERR_VALIDATION, "compensator width must be >= 1");
+  if (workspace_bytes < ffwd_sparse_ffn_workspace_bytes(T, d, f_local, rc_local, k))
+    return fail(FFWD_ERR_VALIDATION, "workspace too small");
+  Carve c(workspace);
+  Ffn w = carve_ffn(c, T, d, f_local, rc_local, k, 0, 4);
+  const int n_blk = (T + kBlockTokens - 1) / kBlockTokens;
+  if (idx == nullptr)  // dense_ffn: identity over every neuron
+    return run_ffn(x_bf16, T, d, wgu_t, wd, f_local, rc_local, w, nullptr, 0, 0, 0, nullptr,
+                   f_local, 0, 0, y, static_cast<cudaStream_t>(stream));
+  return run_ffn(x_bf16, T, d, wgu_t, wd, f_local, rc_local, w, idx, ld_idx, 0, n_blk, counts, k,
+                 idx_per_block ? 0 : 1, has_comp, y, static_cast<cudaStream_t>(stream));
+}
+
+static void layer_split(int T, int k, int f_global, int dense_first_last, int* begin,
+                        int* count) {
+  const int n_blk = (T + kBlockTokens - 1) / kBlockTokens;
+  if (k >= f_global) {  // engine.py:268 full-K shortcut: every block dense
+    *begin = 0;
+    *count = 0;
+  } else if (dense_first_last) {  // engine.py:258-262
+    *begin = 1;
+    *count = n_blk > 2 ? n_blk - 2 : 0;
+  } else {
+    *begin = 0;
+    *count = n_blk;
+  }
+}
+
+static int local_kmax(int k, int f_local) { return k < f_local ? k : f_local; }
+
+size_t ffwd_layer_workspace_bytes(int T, int d, int f_global, int f_local, int rc_local, int r,
+                                  int k, int dense_first_last, int tp_size) {
+  int b0, nb;
+  layer_split(T, k, f_global, dense_first_last, &b0, &nb);
+  (void)tp_size;
+  const int kmax = local_kmax(k, f_local);
+  Carve c(nullptr);
+  carve_pred(c, nb, d, r, f_global);
+  carve_ffn(c, T, d, f_local, rc_local, kmax, nb, rup(kmax, 4));
+  return c.off;
+}
+
+int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t, const void* wd,
+                   int f_local, int rc_local, const float* query, const float* w1,
+                   const float* w2, int r, int f_global, int k, int dense_first_last,
+                   int has_comp, int tp_rank, int tp_size, float* y, int32_t* idx_global,
+                   int ld_idx_global, void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  int rc = check_common(T, d, f_global, k);
+  if (rc) return rc;
+  if ((rc = check_gemm_shapes(d, f_local))) return rc;
+  if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size)
+    return fail(FFWD_ERR_VALIDATION, "bad tensor-parallel rank %d of %d", tp_rank, tp_size);
+  if (f_local != (f_global - tp_rank + tp_size - 1) / tp_size)
+    return fail(FFWD_ERR_VALIDATION, "f_local=%d is not rank %d's strided share of d_ffn=%d",
+                f_local, tp_rank, f_global);
+  if (has_comp && rc_local < 1) return fail(FFWD_ERR_VALIDATION, "compensator width must be >= 1");
+  if (workspace_bytes <
+      ffwd_layer_workspace_bytes(T, d, f_global, f_local, rc_local, r, k, dense_first_last, tp_size))
+    return fail(FFWD_ERR_VALIDATION, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int b0, nb;
+  layer_split(T, k, f_global, dense_first_last, &b0, &nb);
+  const int kmax = local_kmax(k, f_local);
+  Carve c(workspace);
+  Pred p = carve_pred(c, nb, d, r, f_global);
+  Ffn w = carve_ffn(c, T, d, f_local, rc_local, kmax, nb, rup(kmax, 4));
+  if (nb > 0) {
+    if (d % 8 != 0) return fail(FFWD_ERR_UNSUPPORTED, "predictor needs d_model %% 8 == 0");
+    if (idx_global && ld_idx_global < k) return fail(FFWD_ERR_VALIDATION, "ld_idx_global < k");
+    const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));
+    FFWD_CUDA(launch_pool(x_bf16, false, T, d, b0, nb, query, sqrt_d, p.pooled, s), "pool");
+    FFWD_CUDA(launch_gemm_f64acc(p.pooled, w1, p.hidden, nb, d, r, true, s), "w1");
+    FFWD_CUDA(launch_gemm_f64acc(p.hidden, w2, p.scores, nb, r, f_global, false, s), "w2");
+    FFWD_CUDA(launch_topk(p.scores, nb, f_global, k, tp_rank, tp_size, idx_global, ld_idx_global,
+                          w.idx_local, w.ld_local, w.counts, s),
+              "topk");
+  }
+  return run_ffn(x_bf16, T, d, wgu_t, wd, f_local, rc_local, w, w.idx_local, w.ld_local, b0, nb,
+                 tp_size > 1 ? w.counts : nullptr, k, 0, has_comp, y, s);
+}
+
+}  // extern "C"

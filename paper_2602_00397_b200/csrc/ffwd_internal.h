@@ -1,0 +1,98 @@
+// Internal launch interfaces shared by the kernel translation units and the
+// C-ABI shim (capi.cu).  Not part of the public boundary (include/ffwd_b200.h).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace ffwd {
+
+constexpr int kBlockTokens = 128;  // model.py:25 block_size; one UMMA M tile
+
+// Per-block metadata written by the plan kernel (one int4 pair per block).
+struct BlockMeta {
+  int tok0;      // first token row of the block in X / Y
+  int ntok;      // tokens in the block (<= 128; short tail block)
+  int kcount;    // neurons contracted: k_b (sparse) or f_local (dense)
+  int kpad;      // kcount rounded up to 64 (H columns of the FFN part)
+  int comp;      // compensator columns in H (rc rounded to 64) or 0
+  int idx_row;   // row of the index buffer, -1 = identity (dense block)
+  int ktot;      // kpad + comp : K extent of the down projection
+  int n_gu;      // gate/up tiles (128 neurons each) for the up projection
+};
+
+// Tile table entry: block id + packed (kind, offset).  b < 0 = empty slot.
+struct Tile {
+  int b;
+  int n0;    // neuron position (gate/up), comp column (comp) or output column (down)
+  int kind;  // 0 = gate/up, 1 = compensator hidden, 2 = down
+  int pad;
+};
+
+struct PlanCounts {
+  int n_up;    // entries in the up-projection tile table
+  int n_down;  // entries in the down-projection tile table
+  int hcols;   // H row stride actually used (<= the allocated stride)
+  int pad;
+};
+
+// ------------------------------------------------------------------ K1
+cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begin,
+                        int blk_count, const float* query, float sqrt_d, float* pooled,
+                        cudaStream_t s);
+cudaError_t launch_gemm_f64acc(const float* A, const float* B, float* C, int M, int K, int N,
+                               bool relu, cudaStream_t s);
+cudaError_t launch_topk(const float* scores, int n_rows, int f, int k, int tp_rank, int tp_size,
+                        int32_t* idx_global, int ld_global, int32_t* idx_local, int ld_local,
+                        int32_t* counts, cudaStream_t s);
+
+// ------------------------------------------------------------------ K2/K3
+struct PlanArgs {
+  int T, d, f_local, rc_local;
+  int n_blk;
+  int sparse_begin, sparse_count;  // contiguous range of predicted blocks
+  int k_shared;                    // k for sparse blocks when counts == nullptr
+  const int32_t* counts;           // per sparse row counts (TP local) or nullptr
+  int idx_shared;                  // all sparse blocks use index row 0
+  int has_comp;
+  int up_group;                    // blocks per raster group (up projection)
+  int down_group;                  // blocks per raster group (down projection)
+  int bn_down;                     // output columns per down tile
+  int hcols_alloc;
+};
+
+cudaError_t launch_plan(const PlanArgs& a, BlockMeta* meta, Tile* up_tiles, int up_cap,
+                        Tile* down_tiles, int down_cap, PlanCounts* counts, cudaStream_t s);
+
+struct GemmArgs {
+  const void* x;        // bf16 [T x d]
+  const void* wgu_t;    // bf16 [(2 f_local + rc_rows) x d]  gate^T | up^T | Wc1^T
+  int wgu_rows;
+  const void* wd;       // bf16 [(f_local + rc_rows) x d]    W_down | Wc2
+  int wd_rows;
+  void* h;              // bf16 [n_blk*128 x hcols]
+  int hcols;
+  float* y;             // f32 [T x d]
+  int T, d, f_local, n_blk;
+  const int32_t* idx;   // local neuron ids, row stride ld_idx
+  int ld_idx;
+  const BlockMeta* meta;
+  const Tile* up_tiles;
+  int up_cap;
+  const Tile* down_tiles;
+  int down_cap;
+  const PlanCounts* counts;
+  int num_sms;
+  int bn_down;
+};
+
+cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s);
+cudaError_t launch_down_proj(const GemmArgs& a, cudaStream_t s);
+
+// tensor-map encoder (driver entry point resolved once through the runtime)
+CUresult encode_tmap_2d_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows,
+                             uint32_t box_inner, uint32_t box_rows);
+
+}  // namespace ffwd

@@ -1,0 +1,225 @@
+"""Layer-batched FFN branch of the block-wise prefill on the sm_100a kernels.
+
+``sparse_ffn_layer`` is the entry the engine would call once per layer
+instead of the per-block loop of ``engine.py:254-310`` (FFN branch): by
+layer-major equivalence every 128-token block of a layer is
+handled in one stream-ordered sequence of launches:
+
+    pool -> W1 -> W2 -> top-k  (K1, fp64-exact predictor, bit-exact indices)
+    plan                       (device-side tile tables: no host sync)
+    up-proj  (K2)              tcgen05 gather-GEMM, SiLU(g)*u epilogue, comp hidden
+    down-proj (K3)             tcgen05 gather-GEMM, compensator as extra K
+
+Weights are packed once per layer by ``pack_layer`` into the neuron-major
+bf16 layout the kernels gather from (see include/ffwd_b200.h).
+"""
+
+from __future__ import annotations
+
+from collections import OrderedDict
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .compensator import CompensatorParams
+from .errors import ValidationError
+from .predictor import DevicePredictor
+
+BLOCK = 128
+
+
+def _rup(v: int, m: int) -> int:
+    return -(-v // m) * m
+
+
+def shard_neurons(f: int, tp_rank: int, tp_size: int) -> np.ndarray:
+    """Global neuron ids held by a rank: strided {j : j % tp_size == tp_rank}."""
+    if tp_size < 1 or not 0 <= tp_rank < tp_size:
+        raise ValidationError(f"bad tensor-parallel rank {tp_rank} of {tp_size}")
+    return np.arange(tp_rank, f, tp_size, dtype=np.int64)
+
+
+def shard_comp_cols(rc: int, tp_rank: int, tp_size: int) -> tuple[int, int]:
+    """Contiguous compensator-bottleneck columns [lo, hi) of a rank (np.array_split rule)."""
+    base, extra = divmod(rc, tp_size)
+    lo = tp_rank * base + min(tp_rank, extra)
+    return lo, lo + base + (1 if tp_rank < extra else 0)
+
+
+@dataclass
+class PackedLayer:
+    """One rank's FFN (+ compensator) weights in the kernels' neuron-major layout."""
+    wgu_t: torch.Tensor   # bf16 [(2 f_local + roundup(rc_local, 256)) x d]
+    wd: torch.Tensor      # bf16 [(f_local + roundup(rc_local, 64)) x d]
+    d: int
+    f_global: int
+    f_local: int
+    rc_local: int
+    tp_rank: int = 0
+    tp_size: int = 1
+
+    @property
+    def device(self) -> torch.device:
+        return self.wgu_t.device
+
+
+def _as_t(a) -> torch.Tensor:
+    if isinstance(a, torch.Tensor):
+        return a
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float32)))
+
+
+def pack_layer(w_gate, w_up, w_down, comp: CompensatorParams | None = None, device=None,
+               tp_rank: int = 0, tp_size: int = 1) -> PackedLayer:
+    """Build the packed bf16 layout for one rank (one-time layout transform).
+
+    w_gate/w_up (d, f) and w_down (f, d) in the reference orientation
+    (``model.py:79-81``); comp.w1 (d, r'), comp.w2 (r', d) (``compensator.py:25-39``).
+    """
+    dev = torch.device(device) if device is not None else _dev.device_of()
+    g, u, dn = _as_t(w_gate), _as_t(w_up), _as_t(w_down)
+    d, f = g.shape
+    if tuple(u.shape) != (d, f) or tuple(dn.shape) != (f, d):
+        raise ValidationError(f"FFN weights inconsistent: gate {tuple(g.shape)}, "
+                              f"up {tuple(u.shape)}, down {tuple(dn.shape)}")
+    nid = torch.from_numpy(shard_neurons(f, tp_rank, tp_size))
+    f_l = int(nid.numel())
+    rc_l, c1, c2 = 0, None, None
+    if comp is not None:
+        c1, c2 = _as_t(comp.w1), _as_t(comp.w2)
+        rc = c1.shape[1]
+        if c1.shape[0] != d or tuple(c2.shape) != (rc, d):
+            raise ValidationError("compensator shapes inconsistent with the FFN")
+        lo, hi = shard_comp_cols(rc, tp_rank, tp_size)
+        c1, c2 = c1[:, lo:hi], c2[lo:hi]
+        rc_l = hi - lo
+    bf = torch.bfloat16
+    wgu = torch.zeros((2 * f_l + _rup(rc_l, 256), d), dtype=bf, device=dev)
+    wgu[:f_l] = g[:, nid].t().to(dev, bf)
+    wgu[f_l:2 * f_l] = u[:, nid].t().to(dev, bf)
+    wd = torch.zeros((f_l + _rup(rc_l, 64), d), dtype=bf, device=dev)
+    wd[:f_l] = dn[nid].to(dev, bf)
+    if rc_l:
+        wgu[2 * f_l:2 * f_l + rc_l] = c1.t().to(dev, bf)
+        wd[f_l:f_l + rc_l] = c2.to(dev, bf)
+    return PackedLayer(wgu_t=wgu, wd=wd, d=d, f_global=f, f_local=f_l, rc_local=rc_l,
+                       tp_rank=tp_rank, tp_size=tp_size)
+
+
+_pack_cache: "OrderedDict[tuple, tuple]" = OrderedDict()
+
+
+def packed_for(lw, comp, device) -> PackedLayer:
+    """Packed weights for reference-style (numpy) layer weights, cached per object."""
+    key = (id(lw.w_gate), id(lw.w_up), id(lw.w_down), id(comp) if comp is not None else 0,
+           str(device))
+    hit = _pack_cache.get(key)
+    if hit is not None:
+        _pack_cache.move_to_end(key)
+        return hit[0]
+    p = pack_layer(lw.w_gate, lw.w_up, lw.w_down, comp, device=device)
+    _pack_cache[key] = (p, lw, comp)  # keep the sources alive so ids stay unique
+    while len(_pack_cache) > 4:
+        _pack_cache.popitem(last=False)
+    return p
+
+
+def _x_bf16(x, dev) -> torch.Tensor:
+    if isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16:
+        return x.contiguous()
+    return _dev.to_device(x, torch.bfloat16, dev)
+
+
+def run_sparse_ffn(x, packed: PackedLayer, idx: torch.Tensor | None, k: int,
+                   has_comp: bool = False, idx_per_block: bool = True,
+                   counts: torch.Tensor | None = None, out: torch.Tensor | None = None
+                   ) -> torch.Tensor:
+    """FFN over all 128-token blocks of x with given (rank-local) index rows.
+
+    idx None -> dense FFN over every local neuron (``engine.py:127-131``).
+    """
+    dev = packed.device
+    xb = _x_bf16(x, dev)
+    if xb.dim() != 2 or xb.shape[1] != packed.d:
+        raise ValidationError(f"FFN input shape {tuple(xb.shape)}, d_model={packed.d}")
+    T = xb.shape[0]
+    lib = _dev.lib_for(dev)
+    y = out if out is not None else torch.empty((T, packed.d), dtype=torch.float32, device=dev)
+    kk = packed.f_local if idx is None else k
+    ws_n = lib.ffwd_sparse_ffn_workspace_bytes(T, packed.d, packed.f_local, packed.rc_local, kk)
+    ws = _dev.workspace(dev, ws_n)
+    ld = 0 if idx is None else idx.shape[1]
+    _lib.check(lib.ffwd_sparse_ffn(
+        xb.data_ptr(), T, packed.d, packed.wgu_t.data_ptr(), packed.wd.data_ptr(),
+        packed.f_local, packed.rc_local, _dev.ptr(idx), int(idx_per_block), ld,
+        _dev.ptr(counts), kk, int(has_comp and packed.rc_local > 0), y.data_ptr(),
+        ws.data_ptr(), ws.numel(), _dev.stream_handle(dev)), "sparse_ffn")
+    return y
+
+
+def dense_ffn(x, packed: PackedLayer) -> torch.Tensor:
+    """SiLU-gated FFN over all (local) neurons (``engine.py:127-131``), same kernels, identity index."""
+    return run_sparse_ffn(x, packed, None, packed.f_local)
+
+
+def layer_workspace_bytes(T: int, packed: PackedLayer, r: int, k: int,
+                          dense_first_last: bool) -> int:
+    lib = _dev.lib_for(packed.device)
+    return int(lib.ffwd_layer_workspace_bytes(T, packed.d, packed.f_global, packed.f_local,
+                                              packed.rc_local, r, k, int(dense_first_last),
+                                              packed.tp_size))
+
+
+def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
+                     dense_first_last: bool = True, has_comp: bool = True,
+                     out: torch.Tensor | None = None, return_indices: bool = False,
+                     workspace: torch.Tensor | None = None):
+    """One layer's FFN branch over every block of x (T, d); returns y (T, d) f32.
+
+    Semantics of ``engine.py:254-310`` (mode "predicted"): blocks 0 and n-1 run
+    dense when ``dense_first_last`` (``:258-262``); k >= d_ffn runs every block
+    dense with no predictor or compensator (``:268``); otherwise predictor ->
+    top-k -> sparse FFN -> + compensator (``:284-300``).  Under tensor
+    parallelism y is this rank's partial sum (all-reduce it, see ``tp.py``).
+    With ``return_indices`` also returns the (n_predicted, k) global indices.
+    """
+    dev = packed.device
+    xb = _x_bf16(x, dev)
+    T, d = xb.shape
+    if d != packed.d or predictor.d != d or predictor.f != packed.f_global:
+        raise ValidationError(f"layer shapes disagree: x {tuple(xb.shape)}, packed d={packed.d} "
+                              f"f={packed.f_global}, predictor d={predictor.d} f={predictor.f}")
+    if not 1 <= k <= packed.f_global:
+        raise ValidationError(f"k={k} out of range [1, {packed.f_global}]")
+    lib = _dev.lib_for(dev)
+    y = out if out is not None else torch.empty((T, d), dtype=torch.float32, device=dev)
+    n_blk = -(-T // BLOCK)
+    if k >= packed.f_global:
+        n_pred = 0
+    elif dense_first_last:
+        n_pred = max(0, n_blk - 2)
+    else:
+        n_pred = n_blk
+    idx = None
+    if return_indices and n_pred > 0:
+        idx = torch.empty((n_pred, k), dtype=torch.int32, device=dev)
+    ws_n = layer_workspace_bytes(T, packed, predictor.r, k, dense_first_last)
+    ws = workspace if workspace is not None and workspace.numel() >= ws_n else \
+        _dev.workspace(dev, ws_n)
+    _lib.check(lib.ffwd_ffn_layer(
+        xb.data_ptr(), T, d, packed.wgu_t.data_ptr(), packed.wd.data_ptr(), packed.f_local,
+        packed.rc_local, predictor.query.data_ptr(), predictor.w1.data_ptr(),
+        predictor.w2.data_ptr(), predictor.r, predictor.f, k, int(dense_first_last),
+        int(has_comp and packed.rc_local > 0), packed.tp_rank, packed.tp_size, y.data_ptr(),
+        _dev.ptr(idx), k if idx is not None else 0, ws.data_ptr(), ws.numel(),
+        _dev.stream_handle(dev)), "ffn_layer")
+    if return_indices:
+        return y, idx
+    return y
+
+
+def set_raster(up_group: int, down_group: int) -> None:
+    """Blocks per L2 raster group of the up / down gather-GEMMs (tuning knob)."""
+    _lib.check(_lib.load_library().ffwd_set_raster(up_group, down_group), "set_raster")

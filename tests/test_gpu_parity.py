@@ -1,0 +1,246 @@
+"""GPU parity: the sm_100a path against the oracle / the reference's golden vectors.
+
+Bar:
+  * predictor scores and selected indices: bit-exact;
+  * FFN outputs (bf16 operands, f32 accumulation, bf16 hidden):
+        rel-L2 <= 5e-3   and   max|diff| <= 3e-2 * rms(y_ref).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import ffwd_oracle as orc
+from tests.fixtures import golden, load_case
+
+pytestmark = pytest.mark.gpu
+
+REL_L2 = 5e-3
+MAX_REL_RMS = 3e-2
+
+
+@pytest.fixture(scope="module")
+def ff():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2602_00397_b200 as ff
+    from paper_2602_00397_b200 import _lib
+    _lib.require_device(torch.cuda.current_device())
+    return ff
+
+
+def assert_close(got, want, what=""):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    rms = np.sqrt((want ** 2).mean())
+    rel = np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30)
+    mx = np.abs(got - want).max() / max(rms, 1e-30)
+    assert np.isfinite(got).all(), f"{what}: non-finite output"
+    assert rel <= REL_L2, f"{what}: rel-L2 {rel:.3e} > {REL_L2}"
+    assert mx <= MAX_REL_RMS, f"{what}: max|d|/rms {mx:.3e} > {MAX_REL_RMS}"
+    return rel, mx
+
+
+def dev_pred(ff, pred):
+    return ff.DevicePredictor.from_params(ff.PredictorParams(**pred), "cuda")
+
+
+@pytest.mark.parametrize("name", ["tiny_dfl", "tiny_all", "tiny_k25", "cfg1", "l1b", "l8b_pred",
+                                  "qwen8b_pred"])
+def test_predictor_scores_and_indices_bit_exact(ff, name):
+    c = load_case(name)
+    dp = dev_pred(ff, c["pred"])
+    for dtype in (torch.bfloat16, torch.float32):
+        x = torch.from_numpy(c["x"]).to("cuda", dtype)
+        sb = c["sparse_blocks"]
+        if sb.size == 0:
+            continue
+        assert (np.diff(sb) == 1).all()
+        s = ff.predictor_scores(dp, x, int(sb[0]), int(sb.size))
+        got = s.cpu().numpy()
+        np.testing.assert_array_equal(got.view(np.uint32), c["scores"].view(np.uint32))
+        from paper_2602_00397_b200.sparse import topk_device
+        idx = topk_device(s, c["k"]).cpu().numpy()
+        np.testing.assert_array_equal(idx, c["indices"])
+
+
+def test_topk_edge_cases_match_reference(ff):
+    from paper_2602_00397_b200.sparse import topk_device
+    g = golden("topk_edges")
+    for i, k in enumerate(g["k"]):
+        s = g["scores"][g["offs_s"][i]:g["offs_s"][i + 1]]
+        want = g["indices"][g["offs_i"][i]:g["offs_i"][i + 1]]
+        got = topk_device(torch.from_numpy(s.copy()).cuda(), int(k))[0].cpu().numpy()
+        np.testing.assert_array_equal(got, want, err_msg=f"case {i}")
+
+
+def test_topk_large_random_rows(ff):
+    from paper_2602_00397_b200.sparse import topk_device
+    rng = np.random.default_rng(3)
+    for f, k in [(14336, 7168), (12288, 4547), (8192, 2048), (1376, 688), (65536, 1000)]:
+        s = rng.standard_normal((4, f)).astype(np.float32)
+        s[1] = np.round(s[1] * 4) / 4  # many ties
+        s[2, ::7] = -0.0
+        s[3, ::11] = np.nan
+        got = topk_device(torch.from_numpy(s).cuda(), k).cpu().numpy()
+        for r in range(4):
+            np.testing.assert_array_equal(got[r], orc.topk_indices(s[r], k))
+
+
+def test_topk_tp_local_lists(ff):
+    from paper_2602_00397_b200 import _dev, _lib
+    rng = np.random.default_rng(4)
+    f, k = 14336, 7168
+    s = rng.standard_normal((3, f)).astype(np.float32)
+    st = torch.from_numpy(s).cuda()
+    lib = _dev.lib_for(st.device)
+    for tp in (2, 4, 8):
+        for rank in range(tp):
+            loc = torch.full((3, k), -1, dtype=torch.int32, device="cuda")
+            cnt = torch.zeros(3, dtype=torch.int32, device="cuda")
+            _lib.check(lib.ffwd_topk(st.data_ptr(), 3, f, k, rank, tp, None, 0, loc.data_ptr(), k,
+                                     cnt.data_ptr(), _dev.stream_handle(st.device)), "topk")
+            loc, cnt = loc.cpu().numpy(), cnt.cpu().numpy()
+            for r in range(3):
+                full = orc.topk_indices(s[r], k)
+                mine = full[full % tp == rank] // tp
+                assert cnt[r] == mine.size
+                np.testing.assert_array_equal(loc[r, :cnt[r]], mine)
+
+
+def _layer_case(ff, name):
+    c = load_case(name)
+    lw = c["lw"]
+    comp = ff.CompensatorParams(**c["comp"])
+    packed = ff.pack_layer(lw["w_gate"], lw["w_up"], lw["w_down"], comp, device="cuda")
+    return c, packed, dev_pred(ff, c["pred"])
+
+
+@pytest.mark.parametrize("name", ["tiny_dfl", "tiny_all", "tiny_k25", "cfg1", "l1b"])
+def test_ffn_layer_matches_reference(ff, name):
+    c, packed, dp = _layer_case(ff, name)
+    x = torch.from_numpy(c["x"]).to("cuda", torch.bfloat16)
+    y, idx = ff.sparse_ffn_layer(x, packed, dp, c["k"], dense_first_last=c["dense_first_last"],
+                                 return_indices=True)
+    torch.cuda.synchronize()
+    if c["sparse_blocks"].size:
+        np.testing.assert_array_equal(idx.cpu().numpy(), c["indices"])
+    y = y.cpu().numpy()
+    got = y[c["y_rows"]] if "y_rows" in c else y
+    assert_close(got, c["y"], name)
+
+
+def test_dense_layer_and_full_k_shortcut(ff):
+    c, packed, dp = _layer_case(ff, "cfg1")
+    x = torch.from_numpy(c["x"]).to("cuda", torch.bfloat16)
+    lw = c["lw"]
+    want = orc.dense_ffn(c["x"], lw["w_gate"], lw["w_up"], lw["w_down"])
+    assert_close(ff.dense_ffn(x, packed).cpu().numpy(), want, "dense_ffn")
+    # k == d_ffn: every block dense, no predictor, no compensator (engine.py:268)
+    y = ff.sparse_ffn_layer(x, packed, dp, c["f"], dense_first_last=True)
+    assert_close(y.cpu().numpy(), want, "full-k layer")
+
+
+def test_reference_api_drop_in(ff):
+    """predictor_forward / build_mask / select_subweights / sparse_ffn_forward /
+    compensator_forward with numpy in, numpy out (engine.py:286-300 call pattern)."""
+    c = load_case("cfg1")
+    lw = ff.LayerWeights(w_gate=c["lw"]["w_gate"], w_up=c["lw"]["w_up"],
+                         w_down=c["lw"]["w_down"])
+    pred = ff.PredictorParams(**c["pred"])
+    comp = ff.CompensatorParams(**c["comp"])
+    j = int(c["sparse_blocks"][2])
+    xb = c["x"][j * 128:(j + 1) * 128]
+    s = ff.predictor_forward(pred, xb)
+    assert isinstance(s, np.ndarray) and s.dtype == np.float32
+    np.testing.assert_array_equal(s.view(np.uint32), c["scores"][2].view(np.uint32))
+    mask = ff.build_mask(s, c["k"], layer=0, block=j)
+    np.testing.assert_array_equal(mask.indices, c["indices"][2])
+    sub = ff.select_subweights(lw, mask)
+    y = ff.sparse_ffn_forward(xb, sub)
+    want_ffn = orc.sparse_ffn_forward(xb, lw.w_gate, lw.w_up, lw.w_down, mask.indices)
+    assert_close(y, want_ffn, "sparse_ffn_forward")
+    corr = ff.compensator_forward(comp, xb)
+    want_c = orc.compensator_forward(comp.w1, comp.w2, xb)
+    assert_close(corr, want_c, "compensator_forward")
+    yc = ff.apply_compensation(y, corr)
+    rows = c["y_rows"]
+    sel = (rows >= j * 128) & (rows < (j + 1) * 128)
+    assert_close(yc[rows[sel] - j * 128], c["y"][sel], "sparse + compensation vs reference")
+
+
+def test_tensor_parallel_shards_sum_to_full(ff):
+    """TP over d_ffn emulated on one GPU: per-rank partials sum to the TP=1 result."""
+    c = load_case("cfg1")
+    lw, comp = c["lw"], ff.CompensatorParams(**c["comp"])
+    dp = dev_pred(ff, c["pred"])
+    x = torch.from_numpy(c["x"]).to("cuda", torch.bfloat16)
+    full_p = ff.pack_layer(lw["w_gate"], lw["w_up"], lw["w_down"], comp, device="cuda")
+    y1, i1 = ff.sparse_ffn_layer(x, full_p, dp, c["k"], return_indices=True)
+    for tp in (2, 4, 8):
+        acc = torch.zeros_like(y1)
+        for rank in range(tp):
+            p = ff.pack_layer(lw["w_gate"], lw["w_up"], lw["w_down"], comp, device="cuda",
+                              tp_rank=rank, tp_size=tp)
+            yr, ir = ff.sparse_ffn_layer(x, p, dp, c["k"], return_indices=True)
+            assert torch.equal(ir, i1)
+            acc += yr
+        assert_close(acc.cpu().numpy(), y1.cpu().numpy(), f"tp{tp}")
+        rows = c["y_rows"]
+        assert_close(acc.cpu().numpy()[rows], c["y"], f"tp{tp} vs reference")
+
+
+def test_errors_map_to_reference_types(ff):
+    c, packed, dp = _layer_case(ff, "tiny_all")
+    x = torch.from_numpy(c["x"]).to("cuda", torch.bfloat16)
+    with pytest.raises(ff.ValidationError):
+        ff.sparse_ffn_layer(x, packed, dp, 0)
+    with pytest.raises(ff.ValidationError):
+        ff.sparse_ffn_layer(x, packed, dp, c["f"] + 1)
+    with pytest.raises(ff.ValidationError):
+        ff.topk_indices(np.ones(3, np.float32), 4)
+    g = np.zeros((96, 200), np.float32)
+    p96 = ff.pack_layer(g, g, g.T.copy(), None, device="cuda")
+    with pytest.raises(ff.UnsupportedError):
+        ff.dense_ffn(torch.zeros((128, 96), device="cuda"), p96)
+
+
+@pytest.mark.parametrize("shape", [("l8b", 4096, 14336), ("qwen8b", 4096, 12288)])
+def test_full_size_properties(ff, shape):
+    """BASELINE-size layer (T=16K / 8K): sampled blocks vs the oracle, plus
+    size-independent properties (sorted unique indices, finite outputs)."""
+    name, d, f = shape
+    T = 16384 if name == "l8b" else 8192
+    k = orc.budget_to_k(0.5, f)
+    rng = np.random.default_rng(77)
+    lw = orc.random_layer(rng, d, f, 0.02)
+    pred = orc.init_predictor(np.random.default_rng([77, 0]), d, f)
+    comp = {k_: orc.bf16_round(v) for k_, v in
+            orc.init_compensator(np.random.default_rng([78, 0]), d).items()}
+    for key in ("w_gate", "w_up", "w_down"):
+        lw[key] = orc.bf16_round(lw[key])
+    xg = torch.randn((T, d), generator=torch.Generator().manual_seed(5)).to(torch.bfloat16)
+    x_np = xg.float().numpy()
+    packed = ff.pack_layer(lw["w_gate"], lw["w_up"], lw["w_down"], ff.CompensatorParams(**comp),
+                           device="cuda")
+    dp = dev_pred(ff, pred)
+    y, idx = ff.sparse_ffn_layer(xg.cuda(), packed, dp, k, return_indices=True)
+    torch.cuda.synchronize()
+    idx = idx.cpu().numpy()
+    y = y.cpu().numpy()
+    assert np.isfinite(y).all()
+    assert (np.diff(idx, axis=1) > 0).all() and idx.min() >= 0 and idx.max() < f
+    n_blk = T // 128
+    for j in (1, n_blk // 2, n_blk - 2):
+        xb = x_np[j * 128:(j + 1) * 128]
+        s = orc.predictor_forward(pred["query"], pred["w1"], pred["w2"], xb)
+        want_idx = orc.topk_indices(s, k)
+        np.testing.assert_array_equal(idx[j - 1], want_idx)
+    for j in (0, n_blk // 2):  # one dense first block, one predicted block
+        xb = x_np[j * 128:(j + 1) * 128]
+        if j == 0:
+            want = orc.dense_ffn(xb, lw["w_gate"], lw["w_up"], lw["w_down"])
+        else:
+            want = orc.sparse_ffn_forward(xb, lw["w_gate"], lw["w_up"], lw["w_down"], idx[j - 1])
+            want = want + orc.compensator_forward(comp["w1"], comp["w2"], xb)
+        assert_close(y[j * 128:(j + 1) * 128], want, f"{name} block {j}")
