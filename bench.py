@@ -1,0 +1,465 @@
+#!/usr/bin/env python
+"""Benchmark: FastForward prefill-FFN hot path on B200 (BASELINE.json metric).
+
+Metric: "Llama-3.1-8B prefill FFN ms/layer & TTFT at 50% sparsity vs dense, 4K-16K".
+Workload (N=1, BASELINE configs[2] at one GPU): Llama-3.1-8B FFN shape
+(d_model 4096, d_ffn 14336, 32 layers), T = 16384 tokens, 128-token blocks,
+50% keep (k = 7168), dense first/last block, predictor + compensator
+(r 256, r' 512), random-init weights (normal x 0.02, synthetic.py:33-43).
+
+One step = the prefill FFN stack: for each of the 32 layers (own weights, own
+predictor and compensator) the hot path -- predictor -> top-k -> sparse SwiGLU
+FFN + compensator -> residual add (engine.py:254-310 minus attention/RMSNorm) --
+over all 128 blocks.  `value` = device time per step / 32 (ms per layer),
+inputs resident in HBM; `e2e` = the same stack through the public API with the
+prompt's hidden states copied from pinned host memory and the result copied
+back inside the timed region.  Every input (X 128 MiB, weights 361 MiB per
+layer) is larger than L2 and each layer has its own weights, so no L2 flush is
+needed between iterations.
+
+Under torchrun (N > 1): tensor parallel over d_ffn (strided neuron shards,
+replicated predictor, sharded compensator) with one NCCL all-reduce of each
+layer's output; scaling "strong" (total work fixed).
+
+`--impl reference` times the reference's own CPU implementation (the
+unmodified `sparseprefill` package from baseline/_ref when present, else the
+oracle port) on the host cores for a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+METRIC = "Llama-3.1-8B prefill FFN ms/layer & TTFT at 50% sparsity vs dense, 4K–16K"
+CONFIGS = {
+    # name: (d_model, d_ffn, n_layers, T, keep)
+    "8b": (4096, 14336, 32, 16384, 0.5),
+    "1b": (2048, 8192, 16, 4096, 0.5),
+    "qwen8b": (4096, 12288, 36, 8192, 0.5),
+    "cfg1": (512, 1376, 1, 1024, 0.5),
+}
+WORKLOAD_NAMES = {
+    "8b": "Llama-3.1-8B-shape FFN stack (d4096 f14336 x32 layers), T=16384, 50% keep, "
+          "predictor+compensator, dense first/last block",
+    "1b": "Llama-3.2-1B-shape FFN stack (d2048 f8192 x16), T=4096, 50% keep",
+    "qwen8b": "Qwen3-8B-shape FFN stack (d4096 f12288 x36), T=8192, layer-wise schedule, "
+              "budget 0.5",
+    "cfg1": "single SwiGLU FFN layer d512 f1376, T=1024, 50% keep",
+}
+
+
+def load_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return {"hbm": d.get("hbm_gbs", 6551.0), "bf16": d.get("bf16_tflops", 1639.5),
+                "bf16_sus": d.get("bf16_tflops_sustained", 1376.2), "src": "measured"}
+    return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback"}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        loaded = [v for v in sm if v > 0.5 * (mx or 1)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ model
+def make_layers(cfg_name: str, dev, tp_rank: int, tp_size: int, seed: int = 1234):
+    """Random-init packed layers (normal x 0.02) for this rank + per-layer k."""
+    import paper_2602_00397_b200 as ff
+    d, f, L, T, keep = CONFIGS[cfg_name]
+    if cfg_name == "qwen8b":
+        s = np.random.default_rng(seed).random(L) + 0.25  # synthetic importance profile
+        ks = ff.budgets_to_topk(ff.allocate_budgets(s, keep), f)
+    else:
+        ks = [ff.budget_to_k(keep, f)] * L
+    r, rc = ff.default_reduced_dim(d), ff.default_comp_dim(d)
+    layers = []
+    g = torch.Generator(device=dev)
+    for l in range(L):
+        g.manual_seed(seed * 1000 + l)
+
+        def w(*shape):
+            return torch.randn(shape, generator=g, device=dev, dtype=torch.float32).mul_(0.02)
+
+        w_gate, w_up, w_down = w(d, f), w(d, f), w(f, d)
+        comp = ff.CompensatorParams(w1=w(d, rc), w2=w(rc, d))
+        packed = ff.pack_layer(w_gate, w_up, w_down, comp, device=dev, tp_rank=tp_rank,
+                               tp_size=tp_size)
+        dp = ff.DevicePredictor(query=w(d), w1=w(d, r), w2=w(r, f))
+        del w_gate, w_up, w_down
+        layers.append((packed, dp, ks[l]))
+    torch.cuda.synchronize(dev)
+    return layers, ks
+
+
+# ------------------------------------------------------------------ CPU legs
+_CPU_WEIGHTS: dict = {}
+
+
+def cpu_sample(cfg_name: str, impl: str, n_sparse: int = 1, seed: int = 1234):
+    """Time the reference's per-block FFN branch on the host for a bounded sample.
+
+    Returns (ms per layer extrapolated to the full block count, details).
+    impl "reference": the unmodified sparseprefill package (baseline/_ref);
+    impl "port": the oracle restatement (oracle/ffwd_oracle.py).
+    """
+    d, f, L, T, keep = CONFIGS[cfg_name]
+    k = min(f, max(1, int(np.floor(keep * f + 0.5))))
+    from oracle import ffwd_oracle as orc
+    key = (cfg_name, 1234)
+    if key not in _CPU_WEIGHTS:  # generated once; each step draws a fresh block of inputs
+        rng = np.random.default_rng(1234)
+        _CPU_WEIGHTS[key] = (
+            {"w_gate": orc.gaussian(rng, (d, f), 0.02), "w_up": orc.gaussian(rng, (d, f), 0.02),
+             "w_down": orc.gaussian(rng, (f, d), 0.02)},
+            orc.init_predictor(rng, d, f), orc.init_compensator(rng, d))
+    lw, pred, comp = _CPU_WEIGHTS[key]
+    xb = np.random.default_rng(seed).standard_normal((128, d)).astype(np.float32)
+    n_blk = -(-T // 128)
+    if impl == "reference":
+        sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+        from sparseprefill.compensator import (CompensatorParams, apply_compensation,
+                                               compensator_forward)
+        from sparseprefill.engine import dense_ffn
+        from sparseprefill.model import LayerWeights
+        from sparseprefill.predictor import PredictorParams, predictor_forward
+        from sparseprefill.sparse import build_mask, select_subweights, sparse_ffn_forward
+        rlw = LayerWeights(wq=None, wk=None, wv=None, wo=None, w_gate=lw["w_gate"],
+                           w_up=lw["w_up"], w_down=lw["w_down"], attn_norm=None, ffn_norm=None)
+        rp = PredictorParams(**pred)
+        rcp = CompensatorParams(**comp)
+
+        def dense():
+            return dense_ffn(xb, rlw)
+
+        def sparse():  # engine.py:284-300
+            s = predictor_forward(rp, xb)
+            mask = build_mask(s, k)
+            y = sparse_ffn_forward(xb, select_subweights(rlw, mask))
+            return apply_compensation(y, compensator_forward(rcp, xb))
+    else:
+        def dense():
+            return orc.dense_ffn(xb, lw["w_gate"], lw["w_up"], lw["w_down"])
+
+        def sparse():
+            s = orc.predictor_forward(pred["query"], pred["w1"], pred["w2"], xb)
+            idx = orc.topk_indices(s, k)
+            y = orc.sparse_ffn_forward(xb, lw["w_gate"], lw["w_up"], lw["w_down"], idx)
+            return y + orc.compensator_forward(comp["w1"], comp["w2"], xb)
+
+    t0 = time.perf_counter()
+    dense()
+    t_dense = time.perf_counter() - t0
+    ts = []
+    for _ in range(n_sparse):
+        t0 = time.perf_counter()
+        sparse()
+        ts.append(time.perf_counter() - t0)
+    t_sparse = min(ts)
+    n_dense = min(2, n_blk)
+    ms_layer = 1e3 * (n_dense * t_dense + (n_blk - n_dense) * t_sparse)
+    return ms_layer, {"t_dense_block_s": t_dense, "t_sparse_block_s": t_sparse,
+                      "n_blocks": n_blk}
+
+
+def cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    impl = "reference"
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+        import sparseprefill  # noqa: F401
+    except ImportError:
+        impl = "port"
+    d, f, L, T, keep = CONFIGS[args.config]
+    step_ms = []
+    for i in range(args.warmup + args.steps):
+        ms, info = cpu_sample(args.config, impl, n_sparse=1, seed=1234 + i)
+        if i >= args.warmup:
+            step_ms.append(ms)
+    v = float(np.median(step_ms))
+    sample = (f"per step: 1 dense + 1 predicted 128-token block of one layer, extrapolated to "
+              f"{2 if T > 256 else 1} dense + {info['n_blocks'] - 2} predicted blocks")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "ms/layer",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32/f64",
+        "data": "synthetic (random-init weights, N(0,1) inputs)",
+        "config": {"workload": WORKLOAD_NAMES[args.config], "global_batch": 1, "seq_len": T,
+                   "parallelism": "cpu"},
+        "cpu_baseline": {"value": v, "unit": "ms/layer", "cores": cores(),
+                         "kind": "reference" if impl == "reference" else "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "ms/layer", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_gpu(args, rank: int, world: int) -> None:
+    import paper_2602_00397_b200 as ff
+    from paper_2602_00397_b200 import layer as fl
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    peaks = load_peaks()
+    d, f, L, T, keep = CONFIGS[args.config]
+    if args.layers:
+        L = args.layers
+        CONFIGS[args.config] = (d, f, L, T, keep)
+    tp = world
+    layers, ks = make_layers(args.config, dev, rank, tp)
+    n_blk = -(-T // 128)
+    gx = torch.Generator(device=dev)
+    gx.manual_seed(99)
+    x0 = torch.randn((T, d), generator=gx, device=dev).to(torch.bfloat16).float()
+    res = torch.empty_like(x0)
+    xb = torch.empty((T, d), dtype=torch.bfloat16, device=dev)
+    ybuf = torch.empty_like(x0) if tp > 1 else None
+    ws_bytes = max(fl.layer_workspace_bytes(T, p, dp.r, k, True) for p, dp, k in layers)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+
+    def stack(x_src: torch.Tensor):
+        res.copy_(x_src)
+        xb.copy_(x_src)
+        for packed, dp, k in layers:
+            if tp == 1:
+                ff.sparse_ffn_layer(xb, packed, dp, k, out=res, residual=res, x_next=xb,
+                                    workspace=ws)
+            else:
+                ff.sparse_ffn_layer(xb, packed, dp, k, out=ybuf, workspace=ws)
+                torch.distributed.all_reduce(ybuf)
+                res.add_(ybuf)
+                xb.copy_(res)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def timed(fn, steps):
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        barrier()
+        ms = e0.elapsed_time(e1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    # ---- warm-up, then the timed region (kernel event timing on)
+    for _ in range(args.warmup):
+        stack(x0)
+    torch.cuda.synchronize(dev)
+    fl.timing_enable(True)
+    fl.timing_read()
+    with ClockSampler(dev.index) as clk:
+        step_ms = timed(lambda: stack(x0), args.steps)
+    fl.timing_enable(False)
+    stages = fl.timing_read()
+    clocks = clk.summary()
+
+    # ---- e2e through the public API with host buffers
+    host_in = torch.empty((T, d), dtype=torch.float32, pin_memory=True)
+    host_in.copy_(x0.cpu())
+    host_out = torch.empty_like(host_in, pin_memory=True)
+
+    def e2e_step():
+        xd = host_in.to(dev, non_blocking=True)
+        stack(xd)
+        host_out.copy_(res, non_blocking=True)
+
+    for _ in range(1):
+        e2e_step()
+    e2e_ms = timed(e2e_step, max(1, args.steps // 2))
+    h2d = host_in.numel() * 4
+    d2h = host_out.numel() * 4
+
+    # ---- accounting
+    flops_layer = [ff.ffn_path_flops(d, f, T, k) for k in ks]
+    total_flops = sum(flops_layer)
+    value = step_ms / L
+    eff_tflops = total_flops / (step_ms * 1e-3) / 1e12
+    up_ms, up_n = stages["up_proj"]
+    dn_ms, dn_n = stages["down_proj"]
+    rc = ff.default_comp_dim(d)
+    n_pred = max(0, n_blk - 2)
+    up_flops = sum(n_pred * (4 * 128 * d * k + 2 * 128 * d * rc) + 2 * 4 * 128 * d * f
+                   for k in ks) / L
+    up_avg_ms = up_ms / max(1, up_n)
+    achieved = up_flops / tp / (up_avg_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get(args.config, {}).get("up_proj")
+    launches = sum(n for _, n in stages.values())
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "ms/layer", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init normal*0.02 weights, N(0,1) bf16 hidden states)",
+        "config": {"workload": WORKLOAD_NAMES[args.config], "global_batch": 1, "seq_len": T,
+                   "layers": L, "keep": keep, "k_per_layer": ks if args.config == "qwen8b"
+                   else ks[0], "block": 128, "dense_first_last": True,
+                   "parallelism": f"tp{tp}" if tp > 1 else "single",
+                   "l2": "inputs larger than L2 (X 128 MiB, 361 MiB weights per layer, "
+                         "32 distinct layers per step); no flush"},
+        "e2e": {"value": e2e_ms / L, "unit": "ms/layer", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "api": "paper_2602_00397_b200.sparse_ffn_layer (x from pinned host f32)"},
+        "gpu_launches": launches,
+        "effective_tflops": eff_tflops,
+        "roofline": {"kernel": "up_proj (K2 gather-GEMM + SwiGLU)", "bound": "tensor",
+                     "achieved": achieved, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
+                     "frac": achieved / peaks["bf16_sus"],
+                     "frac_of_burst": achieved / peaks["bf16"],
+                     "peak_src": f"{peaks['src']} bf16 sustained (burst {peaks['bf16']})",
+                     "traffic": traffic},
+        "kernels_ms_per_layer": {k_: v[0] / max(1, args.steps * L) for k_, v in stages.items()},
+        "clocks": clocks,
+    }
+
+    # ---- dense baselines on one layer (rank 0 only, single GPU)
+    if world == 1 and not args.skip_dense:
+        packed, dp, k = layers[0]
+        xd = x0.to(torch.bfloat16)
+        own_dense = timed(lambda: ff.dense_ffn(xd, packed), args.steps)
+        # cuBLAS-class dense FFN: [Wg|Wu] fused GEMM, silu*mul, down GEMM (torch.matmul bf16)
+        wgu = packed.wgu_t[:2 * packed.f_local]
+        wdn = packed.wd[:packed.f_local]
+
+        def cublas_ffn():
+            h = xd @ wgu.t()
+            a = torch.nn.functional.silu(h[:, :packed.f_local]) * h[:, packed.f_local:]
+            return a @ wdn
+
+        cublas_ffn()
+        cub = timed(cublas_ffn, args.steps)
+        out["dense"] = {"own_ms_per_layer": own_dense, "cublas_ms_per_layer": cub,
+                        "speedup_vs_cublas_dense": cub / value,
+                        "speedup_vs_own_dense": own_dense / value,
+                        "dense_tflops_cublas": 6 * T * d * f / (cub * 1e-3) / 1e12}
+    del layers
+    torch.cuda.empty_cache()
+
+    # ---- CPU baseline (rank 0, N=1): the oracle port on a bounded sample
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        ms, info = cpu_sample(args.config, "port")
+        out["cpu_baseline"] = {
+            "value": ms, "unit": "ms/layer", "cores": cores(), "kind": "port",
+            "sample": f"oracle port, 1 dense + 1 predicted 128-token block of one layer "
+                      f"(t_dense {info['t_dense_block_s']:.2f}s, t_pred "
+                      f"{info['t_sparse_block_s']:.2f}s), extrapolated to "
+                      f"{info['n_blocks']} blocks"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="8b", choices=sorted(CONFIGS))
+    ap.add_argument("--layers", type=int, default=0, help="override layer count (debug)")
+    ap.add_argument("--skip-dense", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        torch.distributed.init_process_group("nccl")
+    try:
+        run_gpu(args, rank, world)
+    finally:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -113,16 +113,33 @@ FFWD_API int ffwd_sparse_ffn(const void* x_bf16, int T, int d, const void* wgu_t
  * dense first/last block when dense_first_last (engine.py:258-262), dense when
  * k >= f_global (engine.py:268), otherwise predictor -> top-k -> sparse FFN ->
  * compensation (has_comp).  The residual add (engine.py:308) stays with the
- * caller.  idx_global (nullable, [n_sparse x ld_idx_global]) receives the
- * selected global neuron ids of every predicted block.
+ * caller unless `residual` is given: then y = residual + FFN(x) (y may alias
+ * residual), fused into the down-projection epilogue; x_next_bf16 (nullable)
+ * receives bf16(y) as the next layer's input.  Both need tp_size == 1 (under
+ * tensor parallelism the all-reduce comes first).  idx_global (nullable,
+ * [n_sparse x ld_idx_global]) receives the selected global neuron ids of every
+ * predicted block.
  */
 FFWD_API size_t ffwd_layer_workspace_bytes(int T, int d, int f_global, int f_local, int rc_local, int r,
                                   int k, int dense_first_last, int tp_size);
 FFWD_API int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t, const void* wd,
                    int f_local, int rc_local, const float* query, const float* w1,
                    const float* w2, int r, int f_global, int k, int dense_first_last,
-                   int has_comp, int tp_rank, int tp_size, float* y, int32_t* idx_global,
-                   int ld_idx_global, void* workspace, size_t workspace_bytes, void* stream);
+                   int has_comp, int tp_rank, int tp_size, float* y, const float* residual,
+                   void* x_next_bf16, int32_t* idx_global, int ld_idx_global, void* workspace,
+                   size_t workspace_bytes, void* stream);
+
+/*
+ * Per-launch device timing (CUDA events on the launching stream) for the
+ * measurement harness.  Stages: 0 pool, 1 predictor W1, 2 predictor W2,
+ * 3 top-k, 4 plan, 5 up-projection (K2), 6 down-projection (K3).
+ * ffwd_timing_read waits for the recorded events, writes per-stage summed
+ * milliseconds and launch counts, and clears the record.
+ */
+#define FFWD_N_STAGES 7
+FFWD_API int ffwd_timing_enable(int on);
+FFWD_API int ffwd_timing_read(double* ms_out, int* count_out, int n_stages);
+FFWD_API const char* ffwd_stage_name(int stage);
 
 #ifdef __cplusplus
 }

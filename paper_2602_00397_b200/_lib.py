@@ -40,7 +40,11 @@ SIGNATURES = {
                                              _c_int, _c_int, _c_int]),
     "ffwd_ffn_layer": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _vp, _vp, _vp,
                                 _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp,
-                                _vp, _c_int, _vp, _c_size, _vp]),
+                                _vp, _vp, _vp, _c_int, _vp, _c_size, _vp]),
+    "ffwd_timing_enable": (_c_int, [_c_int]),
+    "ffwd_timing_read": (_c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_c_int),
+                                  _c_int]),
+    "ffwd_stage_name": (ctypes.c_char_p, [_c_int]),
 }
 
 _lib = None

@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/ffwd_b200.h"
 #include "ffwd_internal.h"
@@ -41,6 +42,46 @@ int cuda_fail(cudaError_t e, const char* where) {
   } while (0)
 
 int rup(int v, int m) { return (v + m - 1) / m * m; }
+
+// ---- optional per-launch event timing (measurement harness only)
+enum Stage { kPool = 0, kW1, kW2, kTopk, kPlan, kUp, kDown, kNumStages };
+const char* kStageNames[kNumStages] = {"pool", "predictor_w1", "predictor_w2", "topk",
+                                       "plan", "up_proj", "down_proj"};
+bool g_timing = false;
+struct Rec {
+  int stage;
+  cudaEvent_t a, b;
+};
+std::vector<Rec> g_recs;
+std::vector<cudaEvent_t> g_event_pool;
+
+cudaEvent_t take_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct StageTimer {
+  Rec r{-1, nullptr, nullptr};
+  cudaStream_t s;
+  StageTimer(int stage, cudaStream_t st) : s(st) {
+    if (!g_timing) return;
+    r.stage = stage;
+    r.a = take_event();
+    r.b = take_event();
+    cudaEventRecord(r.a, s);
+  }
+  ~StageTimer() {
+    if (r.stage < 0) return;
+    cudaEventRecord(r.b, s);
+    g_recs.push_back(r);
+  }
+};
 size_t al(size_t v) { return (v + 255) & ~size_t(255); }
 
 int num_sms() {
@@ -123,7 +164,7 @@ int check_common(int T, int d, int f, int k) {
 int run_ffn(const void* x, int T, int d, const void* wgu_t, const void* wd, int f_local,
             int rc_local, const Ffn& w, const int32_t* idx, int ld_idx, int sparse_begin,
             int sparse_count, const int32_t* counts, int k_shared, int idx_shared, int has_comp,
-            float* y, cudaStream_t s) {
+            float* y, const float* residual, void* x_next, cudaStream_t s) {
   const int n_blk = (T + kBlockTokens - 1) / kBlockTokens;
   PlanArgs pa{};
   pa.T = T;
@@ -141,7 +182,10 @@ int run_ffn(const void* x, int T, int d, const void* wgu_t, const void* wd, int 
   pa.down_group = g_down_group;
   pa.bn_down = bn_for(d);
   pa.hcols_alloc = w.hcols;
-  FFWD_CUDA(launch_plan(pa, w.meta, w.up, w.up_cap, w.down, w.down_cap, w.pc, s), "plan");
+  {
+    StageTimer tm(kPlan, s);
+    FFWD_CUDA(launch_plan(pa, w.meta, w.up, w.up_cap, w.down, w.down_cap, w.pc, s), "plan");
+  }
   GemmArgs ga{};
   ga.x = x;
   ga.wgu_t = wgu_t;
@@ -151,6 +195,8 @@ int run_ffn(const void* x, int T, int d, const void* wgu_t, const void* wd, int 
   ga.h = w.h;
   ga.hcols = w.hcols;
   ga.y = y;
+  ga.residual = residual;
+  ga.x_next = x_next;
   ga.T = T;
   ga.d = d;
   ga.f_local = f_local;
@@ -165,8 +211,14 @@ int run_ffn(const void* x, int T, int d, const void* wgu_t, const void* wd, int 
   ga.counts = w.pc;
   ga.num_sms = num_sms();
   ga.bn_down = bn_for(d);
-  FFWD_CUDA(launch_up_proj(ga, s), "up_proj");
-  FFWD_CUDA(launch_down_proj(ga, s), "down_proj");
+  {
+    StageTimer tm(kUp, s);
+    FFWD_CUDA(launch_up_proj(ga, s), "up_proj");
+  }
+  {
+    StageTimer tm(kDown, s);
+    FFWD_CUDA(launch_down_proj(ga, s), "down_proj");
+  }
   return FFWD_OK;
 }
 
@@ -289,9 +341,10 @@ int ffwd_sparse_ffn(const void* x_bf16, int T, int d, const void* wgu_t, const v
   const int n_blk = (T + kBlockTokens - 1) / kBlockTokens;
   if (idx == nullptr)  // dense_ffn: identity over every neuron
     return run_ffn(x_bf16, T, d, wgu_t, wd, f_local, rc_local, w, nullptr, 0, 0, 0, nullptr,
-                   f_local, 0, 0, y, static_cast<cudaStream_t>(stream));
+                   f_local, 0, 0, y, nullptr, nullptr, static_cast<cudaStream_t>(stream));
   return run_ffn(x_bf16, T, d, wgu_t, wd, f_local, rc_local, w, idx, ld_idx, 0, n_blk, counts, k,
-                 idx_per_block ? 0 : 1, has_comp, y, static_cast<cudaStream_t>(stream));
+                 idx_per_block ? 0 : 1, has_comp, y, nullptr, nullptr,
+                 static_cast<cudaStream_t>(stream));
 }
 
 static void layer_split(int T, int k, int f_global, int dense_first_last, int* begin,
@@ -326,8 +379,9 @@ size_t ffwd_layer_workspace_bytes(int T, int d, int f_global, int f_local, int r
 int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t, const void* wd,
                    int f_local, int rc_local, const float* query, const float* w1,
                    const float* w2, int r, int f_global, int k, int dense_first_last,
-                   int has_comp, int tp_rank, int tp_size, float* y, int32_t* idx_global,
-                   int ld_idx_global, void* workspace, size_t workspace_bytes, void* stream) {
+                   int has_comp, int tp_rank, int tp_size, float* y, const float* residual,
+                   void* x_next_bf16, int32_t* idx_global, int ld_idx_global, void* workspace,
+                   size_t workspace_bytes, void* stream) {
   g_err.clear();
   int rc = check_common(T, d, f_global, k);
   if (rc) return rc;
@@ -338,6 +392,8 @@ int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t, const vo
     return fail(FFWD_ERR_VALIDATION, "f_local=%d is not rank %d's strided share of d_ffn=%d",
                 f_local, tp_rank, f_global);
   if (has_comp && rc_local < 1) return fail(FFWD_ERR_VALIDATION, "compensator width must be >= 1");
+  if ((residual || x_next_bf16) && tp_size != 1)
+    return fail(FFWD_ERR_VALIDATION, "fused residual needs tp_size == 1 (all-reduce first)");
   if (workspace_bytes <
       ffwd_layer_workspace_bytes(T, d, f_global, f_local, rc_local, r, k, dense_first_last, tp_size))
     return fail(FFWD_ERR_VALIDATION, "workspace too small");
@@ -352,15 +408,59 @@ int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t, const vo
     if (d % 8 != 0) return fail(FFWD_ERR_UNSUPPORTED, "predictor needs d_model %% 8 == 0");
     if (idx_global && ld_idx_global < k) return fail(FFWD_ERR_VALIDATION, "ld_idx_global < k");
     const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));
-    FFWD_CUDA(launch_pool(x_bf16, false, T, d, b0, nb, query, sqrt_d, p.pooled, s), "pool");
-    FFWD_CUDA(launch_gemm_f64acc(p.pooled, w1, p.hidden, nb, d, r, true, s), "w1");
-    FFWD_CUDA(launch_gemm_f64acc(p.hidden, w2, p.scores, nb, r, f_global, false, s), "w2");
-    FFWD_CUDA(launch_topk(p.scores, nb, f_global, k, tp_rank, tp_size, idx_global, ld_idx_global,
-                          w.idx_local, w.ld_local, w.counts, s),
-              "topk");
+    {
+      StageTimer tm(kPool, s);
+      FFWD_CUDA(launch_pool(x_bf16, false, T, d, b0, nb, query, sqrt_d, p.pooled, s), "pool");
+    }
+    {
+      StageTimer tm(kW1, s);
+      FFWD_CUDA(launch_gemm_f64acc(p.pooled, w1, p.hidden, nb, d, r, true, s), "w1");
+    }
+    {
+      StageTimer tm(kW2, s);
+      FFWD_CUDA(launch_gemm_f64acc(p.hidden, w2, p.scores, nb, r, f_global, false, s), "w2");
+    }
+    {
+      StageTimer tm(kTopk, s);
+      FFWD_CUDA(launch_topk(p.scores, nb, f_global, k, tp_rank, tp_size, idx_global,
+                            ld_idx_global, w.idx_local, w.ld_local, w.counts, s),
+                "topk");
+    }
   }
   return run_ffn(x_bf16, T, d, wgu_t, wd, f_local, rc_local, w, w.idx_local, w.ld_local, b0, nb,
-                 tp_size > 1 ? w.counts : nullptr, k, 0, has_comp, y, s);
+                 tp_size > 1 ? w.counts : nullptr, k, 0, has_comp, y, residual, x_next_bf16, s);
+}
+
+int ffwd_timing_enable(int on) {
+  g_timing = on != 0;
+  return FFWD_OK;
+}
+
+int ffwd_timing_read(double* ms_out, int* count_out, int n_stages) {
+  g_err.clear();
+  for (int i = 0; i < n_stages; ++i) {
+    if (ms_out) ms_out[i] = 0.0;
+    if (count_out) count_out[i] = 0;
+  }
+  int rc = FFWD_OK;
+  for (const Rec& r : g_recs) {
+    float ms = 0.f;
+    cudaError_t e = cudaEventSynchronize(r.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
+    if (e != cudaSuccess && rc == FFWD_OK) rc = cuda_fail(e, "timing_read");
+    if (r.stage < n_stages) {
+      if (ms_out) ms_out[r.stage] += ms;
+      if (count_out) count_out[r.stage] += 1;
+    }
+    g_event_pool.push_back(r.a);
+    g_event_pool.push_back(r.b);
+  }
+  g_recs.clear();
+  return rc;
+}
+
+const char* ffwd_stage_name(int stage) {
+  return (stage >= 0 && stage < kNumStages) ? kStageNames[stage] : "";
 }
 
 }  // extern "C"

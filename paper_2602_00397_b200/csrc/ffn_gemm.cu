@@ -474,7 +474,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&sm.bar->tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tb = tmem + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
-      float* yrow = a.y + static_cast<size_t>(m.tok0 + row) * a.d + tl.n0;
+      const size_t row_off = static_cast<size_t>(m.tok0 + row) * a.d + tl.n0;
+      float* yrow = a.y + row_off;
       const bool live = row < m.ntok;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
@@ -482,11 +483,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld32(tb + c, v);
         tmem_ld_wait();
         if (live) {
+          float o[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = __uint_as_float(v[j]);
+          if (a.residual) {  // fused residual add (engine.py:308)
+            const float4* res = reinterpret_cast<const float4*>(a.residual + row_off + c);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 r = res[j];
+              o[4 * j] += r.x;
+              o[4 * j + 1] += r.y;
+              o[4 * j + 2] += r.z;
+              o[4 * j + 3] += r.w;
+            }
+          }
           float4* dst = reinterpret_cast<float4*>(yrow + c);
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            dst[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                 __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+            dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+          if (a.x_next) {  // next layer's bf16 input, written once here
+            uint4* xn = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.x_next) +
+                                                 row_off + c);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              xn[j] = make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]),
+                                 pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
+                                 pack_bf16x2(o[8 * j + 4], o[8 * j + 5]),
+                                 pack_bf16x2(o[8 * j + 6], o[8 * j + 7]));
+          }
         }
       }
       tc_fence_before();

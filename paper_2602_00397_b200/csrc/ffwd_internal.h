@@ -75,6 +75,8 @@ struct GemmArgs {
   void* h;              // bf16 [n_blk*128 x hcols]
   int hcols;
   float* y;             // f32 [T x d]
+  const float* residual;  // nullable: y = residual + FFN (may alias y; engine.py:308)
+  void* x_next;         // nullable: bf16 copy of y for the next layer's input
   int T, d, f_local, n_blk;
   const int32_t* idx;   // local neuron ids, row stride ld_idx
   int ld_idx;

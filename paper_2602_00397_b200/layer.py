@@ -175,7 +175,8 @@ def layer_workspace_bytes(T: int, packed: PackedLayer, r: int, k: int,
 def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
                      dense_first_last: bool = True, has_comp: bool = True,
                      out: torch.Tensor | None = None, return_indices: bool = False,
-                     workspace: torch.Tensor | None = None):
+                     workspace: torch.Tensor | None = None,
+                     residual: torch.Tensor | None = None, x_next: torch.Tensor | None = None):
     """One layer's FFN branch over every block of x (T, d); returns y (T, d) f32.
 
     Semantics of ``engine.py:254-310`` (mode "predicted"): blocks 0 and n-1 run
@@ -184,6 +185,9 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
     top-k -> sparse FFN -> + compensator (``:284-300``).  Under tensor
     parallelism y is this rank's partial sum (all-reduce it, see ``tp.py``).
     With ``return_indices`` also returns the (n_predicted, k) global indices.
+    ``residual`` (f32 (T, d), may be ``out``) fuses the residual add of
+    ``engine.py:308`` into the down-projection epilogue; ``x_next`` (bf16 (T, d))
+    receives bf16(y) as the next layer's input (tp_size == 1 only).
     """
     dev = packed.device
     xb = _x_bf16(x, dev)
@@ -213,7 +217,7 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
         packed.rc_local, predictor.query.data_ptr(), predictor.w1.data_ptr(),
         predictor.w2.data_ptr(), predictor.r, predictor.f, k, int(dense_first_last),
         int(has_comp and packed.rc_local > 0), packed.tp_rank, packed.tp_size, y.data_ptr(),
-        _dev.ptr(idx), k if idx is not None else 0, ws.data_ptr(), ws.numel(),
+        _dev.ptr(residual), _dev.ptr(x_next), _dev.ptr(idx), k if idx is not None else 0, ws.data_ptr(), ws.numel(),
         _dev.stream_handle(dev)), "ffn_layer")
     if return_indices:
         return y, idx
@@ -223,3 +227,21 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
 def set_raster(up_group: int, down_group: int) -> None:
     """Blocks per L2 raster group of the up / down gather-GEMMs (tuning knob)."""
     _lib.check(_lib.load_library().ffwd_set_raster(up_group, down_group), "set_raster")
+
+
+STAGES = ("pool", "predictor_w1", "predictor_w2", "topk", "plan", "up_proj", "down_proj")
+
+
+def timing_enable(on: bool = True) -> None:
+    """Record CUDA events around every kernel launch of ``sparse_ffn_layer``."""
+    _lib.load_library().ffwd_timing_enable(int(on))
+
+
+def timing_read() -> dict:
+    """{stage: (summed ms, launches)} since the last read (waits for the events)."""
+    import ctypes
+    n = len(STAGES)
+    ms = (ctypes.c_double * n)()
+    cnt = (ctypes.c_int * n)()
+    _lib.check(_lib.load_library().ffwd_timing_read(ms, cnt, n), "timing_read")
+    return {STAGES[i]: (ms[i], cnt[i]) for i in range(n)}
