@@ -66,7 +66,7 @@ FFWD_API int ffwd_set_raster(int up_group, int down_group);
  * x: [T x d] f32 (x_is_f32 = 1) or bf16; query f32 [d]; w1 f32 [d x r];
  * w2 f32 [r x f]; scores f32 [blk_count x f].
  */
-FFWD_API size_t ffwd_predictor_workspace_bytes(int blk_count, int d, int r);
+FFWD_API size_t ffwd_predictor_workspace_bytes(int blk_count, int d, int r, int f);
 FFWD_API int ffwd_predictor_forward(const void* x, int x_is_f32, int T, int d, int blk_begin,
                            int blk_count, const float* query, const float* w1, const float* w2,
                            int r, int f, float* scores, void* workspace,

@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -107,17 +108,43 @@ struct Carve {
 };
 
 struct Pred {
+  float* logits;
   float* pooled;
   float* hidden;
-  float* scores;
+  double* partial;
+  float* scores;  // only carved when with_scores
 };
 
-Pred carve_pred(Carve& c, int nb, int d, int r, int f) {
+Pred carve_pred(Carve& c, int nb, int d, int r, int f, bool with_scores) {
   Pred p;
+  p.logits = c.take<float>(static_cast<size_t>(nb) * kBlockTokens);
   p.pooled = c.take<float>(static_cast<size_t>(nb) * d);
   p.hidden = c.take<float>(static_cast<size_t>(nb) * r);
-  p.scores = c.take<float>(static_cast<size_t>(nb) * f);
+  const size_t part = std::max(gemm_f64acc_partial_bytes(nb, d, r),
+                               gemm_f64acc_partial_bytes(nb, r, f));
+  p.partial = c.take<double>(part / sizeof(double));
+  p.scores = with_scores ? c.take<float>(static_cast<size_t>(nb) * f) : nullptr;
   return p;
+}
+
+int run_predictor(const void* x, bool x_is_f32, int T, int d, int b0, int nb, const float* query,
+                  const float* w1, const float* w2, int r, int f, const Pred& p, float* scores,
+                  cudaStream_t s) {
+  const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));  // predictor.py:76
+  {
+    StageTimer tm(kPool, s);
+    FFWD_CUDA(launch_pool(x, x_is_f32, T, d, b0, nb, query, sqrt_d, p.logits, p.pooled, s),
+              "pool");
+  }
+  {
+    StageTimer tm(kW1, s);
+    FFWD_CUDA(launch_gemm_f64acc(p.pooled, w1, p.hidden, nb, d, r, true, p.partial, s), "w1");
+  }
+  {
+    StageTimer tm(kW2, s);
+    FFWD_CUDA(launch_gemm_f64acc(p.hidden, w2, scores, nb, r, f, false, p.partial, s), "w2");
+  }
+  return FFWD_OK;
 }
 
 struct Ffn {
@@ -255,9 +282,9 @@ int ffwd_set_raster(int up_group, int down_group) {
   return FFWD_OK;
 }
 
-size_t ffwd_predictor_workspace_bytes(int blk_count, int d, int r) {
+size_t ffwd_predictor_workspace_bytes(int blk_count, int d, int r, int f) {
   Carve c(nullptr);
-  carve_pred(c, blk_count, d, r, 0);
+  carve_pred(c, blk_count, d, r, f, false);
   return c.off;
 }
 
@@ -274,17 +301,12 @@ int ffwd_predictor_forward(const void* x, int x_is_f32, int T, int d, int blk_be
   if (blk_begin < 0 || blk_count < 0 || blk_begin + blk_count > n_blk)
     return fail(FFWD_ERR_VALIDATION, "block range [%d, %d) outside [0, %d)", blk_begin,
                 blk_begin + blk_count, n_blk);
-  if (workspace_bytes < ffwd_predictor_workspace_bytes(blk_count, d, r))
+  if (workspace_bytes < ffwd_predictor_workspace_bytes(blk_count, d, r, f))
     return fail(FFWD_ERR_VALIDATION, "workspace too small");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   Carve c(workspace);
-  Pred p = carve_pred(c, blk_count, d, r, 0);
-  const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));
-  FFWD_CUDA(launch_pool(x, x_is_f32 != 0, T, d, blk_begin, blk_count, query, sqrt_d, p.pooled, s),
-            "pool");
-  FFWD_CUDA(launch_gemm_f64acc(p.pooled, w1, p.hidden, blk_count, d, r, true, s), "w1");
-  FFWD_CUDA(launch_gemm_f64acc(p.hidden, w2, scores, blk_count, r, f, false, s), "w2");
-  return FFWD_OK;
+  Pred p = carve_pred(c, blk_count, d, r, f, false);
+  return run_predictor(x, x_is_f32 != 0, T, d, blk_begin, blk_count, query, w1, w2, r, f, p,
+                       scores, static_cast<cudaStream_t>(stream));
 }
 
 int ffwd_topk(const float* scores, int n_rows, int f, int k, int tp_rank, int tp_size,
@@ -307,11 +329,10 @@ int ffwd_predict_topk(const void* x, int x_is_f32, int T, int d, int blk_begin, 
                       int tp_rank, int tp_size, int32_t* idx_global, int ld_global,
                       int32_t* idx_local, int ld_local, int32_t* counts, void* workspace,
                       size_t workspace_bytes, void* stream) {
-  const size_t need = ffwd_predictor_workspace_bytes(blk_count, d, r) +
-                      al(static_cast<size_t>(blk_count) * f * sizeof(float));
+  const size_t pred_bytes = ffwd_predictor_workspace_bytes(blk_count, d, r, f);
+  const size_t need = pred_bytes + al(static_cast<size_t>(blk_count) * f * sizeof(float));
   if (workspace_bytes < need) return fail(FFWD_ERR_VALIDATION, "workspace too small");
-  float* scores = reinterpret_cast<float*>(static_cast<char*>(workspace) +
-                                           ffwd_predictor_workspace_bytes(blk_count, d, r));
+  float* scores = reinterpret_cast<float*>(static_cast<char*>(workspace) + pred_bytes);
   int rc = ffwd_predictor_forward(x, x_is_f32, T, d, blk_begin, blk_count, query, w1, w2, r, f,
                                   scores, workspace, workspace_bytes, stream);
   if (rc != FFWD_OK) return rc;
@@ -371,7 +392,7 @@ size_t ffwd_layer_workspace_bytes(int T, int d, int f_global, int f_local, int r
   (void)tp_size;
   const int kmax = local_kmax(k, f_local);
   Carve c(nullptr);
-  carve_pred(c, nb, d, r, f_global);
+  carve_pred(c, nb, d, r, f_global, true);
   carve_ffn(c, T, d, f_local, rc_local, kmax, nb, rup(kmax, 4));
   return c.off;
 }
@@ -402,24 +423,13 @@ int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t, const vo
   layer_split(T, k, f_global, dense_first_last, &b0, &nb);
   const int kmax = local_kmax(k, f_local);
   Carve c(workspace);
-  Pred p = carve_pred(c, nb, d, r, f_global);
+  Pred p = carve_pred(c, nb, d, r, f_global, true);
   Ffn w = carve_ffn(c, T, d, f_local, rc_local, kmax, nb, rup(kmax, 4));
   if (nb > 0) {
     if (d % 8 != 0) return fail(FFWD_ERR_UNSUPPORTED, "predictor needs d_model %% 8 == 0");
     if (idx_global && ld_idx_global < k) return fail(FFWD_ERR_VALIDATION, "ld_idx_global < k");
-    const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));
-    {
-      StageTimer tm(kPool, s);
-      FFWD_CUDA(launch_pool(x_bf16, false, T, d, b0, nb, query, sqrt_d, p.pooled, s), "pool");
-    }
-    {
-      StageTimer tm(kW1, s);
-      FFWD_CUDA(launch_gemm_f64acc(p.pooled, w1, p.hidden, nb, d, r, true, s), "w1");
-    }
-    {
-      StageTimer tm(kW2, s);
-      FFWD_CUDA(launch_gemm_f64acc(p.hidden, w2, p.scores, nb, r, f_global, false, s), "w2");
-    }
+    rc = run_predictor(x_bf16, false, T, d, b0, nb, query, w1, w2, r, f_global, p, p.scores, s);
+    if (rc) return rc;
     {
       StageTimer tm(kTopk, s);
       FFWD_CUDA(launch_topk(p.scores, nb, f_global, k, tp_rank, tp_size, idx_global,

@@ -1,0 +1,192 @@
+// K3: down projection + low-rank compensator as one tcgen05 gather-GEMM.
+//
+//   Y_b = [H_b | C_b] . [W_down[idx_b, :] ; Wc2]
+//   (sparse.py:91 down matmul + compensator.py:52-66: silu(x Wc1) Wc2 added to
+//   the output -- here simply r' extra K iterations into the same TMEM
+//   accumulator, so the correction is fused into the down-projection accumulate)
+//
+// A = H_b (128 x 64 per stage, K-major) by 2-D TMA; B = the stage's 64 K rows
+// (selected neurons, then compensator rows) of [W_down ; Wc2] (bf16, d
+// contiguous = MN-major) by TMA tile::gather4 in BN/64 column atoms; D = 128 x BN
+// f32 in TMEM.  Epilogue: optional residual add (engine.py:308) and optional
+// bf16 copy for the next layer's input, f32 Y stores.
+#include "gemm_sm100.cuh"
+
+namespace ffwd {
+
+namespace {
+
+using namespace gemm;
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    down_proj_kernel(const __grid_constant__ CUtensorMap tm_h,
+                     const __grid_constant__ CUtensorMap tm_w, GemmArgs a) {
+  constexpr int kBBytes = BK * BN * 2;
+  constexpr int kChunks = BN / 64;            // 64-column (128 B) atoms along N
+  constexpr uint32_t kLbo = (BK / 8) * 1024;  // MN-direction atom stride
+  extern __shared__ uint8_t smem_raw[];
+  Smem<kBBytes> sm(smem_raw);
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_h);
+    tma_prefetch_desc(&tm_w);
+  }
+  prologue(sm, warp);
+  const uint32_t tmem = sm.bar->tmem_base;
+  const int n_tiles = a.counts->n_down;
+
+  if (warp < kProducerWarps) {
+    // ---------------- producers: warp w gathers K rows [16w, 16w + 16) of every stage
+    const uint64_t pol_h = policy_evict_last();
+    const uint64_t pol_w = policy_evict_normal();
+    int* rows = sm.bar->rows[warp];
+    uint32_t stage = 0, phase = 0;
+    const uint32_t bytes = 16 * BN * 2 + (warp == 0 ? kABytes : 0);
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const Tile tl = a.down_tiles[t];
+      if (tl.b < 0) continue;
+      const BlockMeta m = a.meta[tl.b];
+      const int nk = m.ktot / BK;
+      auto row_of = [&](int kb) -> int {
+        const int p = kb * BK + 16 * warp + static_cast<int>(lane & 15);
+        return p < m.kpad ? neuron_at(m, a.idx, a.ld_idx, p) : a.f_local + (p - m.kpad);
+      };
+      int next = row_of(0);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int cur = next;
+        if (kb + 1 < nk) next = row_of(kb + 1);  // prefetch: consumed next iteration
+        if (lane < 16) rows[lane] = cur;
+        __syncwarp();
+        if (lane == 0) {
+          mbar_wait(&sm.bar->empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&sm.bar->full[stage], bytes);
+          if (warp == 0)
+            tma_load_2d(&tm_h, &sm.bar->full[stage], sm.a_stage(stage), kb * BK,
+                        tl.b * kBlockTokens, pol_h);
+          const int4* rq = reinterpret_cast<const int4*>(rows);
+          uint8_t* dst = sm.b_stage(stage) + warp * 2 * 1024;  // K rows 16w.. = 2 atoms
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int4 r = rq[q];
+#pragma unroll
+            for (int c = 0; c < kChunks; ++c)
+              tma_gather4(&tm_w, &sm.bar->full[stage],
+                          dst + c * kLbo + (q >> 1) * 1024 + (q & 1) * 512, tl.n0 + c * 64, r.x,
+                          r.y, r.z, r.w, pol_w);
+          }
+        }
+        __syncwarp();
+        advance(stage, phase);
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, true);
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const Tile tl = a.down_tiles[t];
+        if (tl.b < 0) continue;
+        const BlockMeta m = a.meta[tl.b];
+        mbar_wait_sleep(&sm.bar->tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        mma_tile(sm, tmem + acc * BN, m.ktot / BK, idesc, kLbo, 1024, 2048, stage, phase);
+        umma_commit(&sm.bar->tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue
+    const int ew = warp - kEpiWarp0;
+    const int row = ew * 32 + static_cast<int>(lane);
+    uint32_t acc = 0, acc_phase = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const Tile tl = a.down_tiles[t];
+      if (tl.b < 0) continue;
+      const BlockMeta m = a.meta[tl.b];
+      mbar_wait_sleep(&sm.bar->tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tb = tmem + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
+      const size_t row_off = static_cast<size_t>(m.tok0 + row) * a.d + tl.n0;
+      const bool live = row < m.ntok;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t v[32];
+        tmem_ld32(tb + c, v);
+        tmem_ld_wait();
+        if (live) {
+          float o[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) o[j] = __uint_as_float(v[j]);
+          if (a.residual) {  // fused residual add (engine.py:308)
+            const float4* res = reinterpret_cast<const float4*>(a.residual + row_off + c);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 r = res[j];
+              o[4 * j] += r.x;
+              o[4 * j + 1] += r.y;
+              o[4 * j + 2] += r.z;
+              o[4 * j + 3] += r.w;
+            }
+          }
+          float4* dst = reinterpret_cast<float4*>(a.y + row_off + c);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+          if (a.x_next) {  // next layer's bf16 input
+            uint4* xn = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.x_next) +
+                                                 row_off + c);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              xn[j] = make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]),
+                                 pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
+                                 pack_bf16x2(o[8 * j + 4], o[8 * j + 5]),
+                                 pack_bf16x2(o[8 * j + 6], o[8 * j + 7]));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&sm.bar->tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  teardown(sm, warp);
+}
+
+template <int BN>
+cudaError_t launch_bn(const GemmArgs& a, cudaStream_t s) {
+  CUtensorMap th, tw;
+  if (encode_tmap_2d_bf16(&th, a.h, a.hcols, static_cast<uint64_t>(a.n_blk) * BM, BK, BM) !=
+      CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  if (encode_tmap_2d_bf16(&tw, a.wd, a.d, a.wd_rows, 64, 1) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  constexpr size_t smem = smem_bytes<BK * BN * 2>();
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(down_proj_kernel<BN>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int grid = a.num_sms < a.down_cap ? a.num_sms : a.down_cap;
+  down_proj_kernel<BN><<<grid, kThreads, smem, s>>>(th, tw, a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_down_proj(const GemmArgs& a, cudaStream_t s) {
+  switch (a.bn_down) {
+    case 256: return launch_bn<256>(a, s);
+    case 128: return launch_bn<128>(a, s);
+    case 64: return launch_bn<64>(a, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace ffwd

@@ -40,10 +40,13 @@ struct PlanCounts {
 
 // ------------------------------------------------------------------ K1
 cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begin,
-                        int blk_count, const float* query, float sqrt_d, float* pooled,
-                        cudaStream_t s);
+                        int blk_count, const float* query, float sqrt_d, float* logits,
+                        float* pooled, cudaStream_t s);
+// f64-accumulated f32 GEMM; `partial` (nullable, gemm_f64acc_partial_bytes) enables split-K.
+int gemm_f64acc_splits(int M, int K, int N);
+size_t gemm_f64acc_partial_bytes(int M, int K, int N);
 cudaError_t launch_gemm_f64acc(const float* A, const float* B, float* C, int M, int K, int N,
-                               bool relu, cudaStream_t s);
+                               bool relu, double* partial, cudaStream_t s);
 cudaError_t launch_topk(const float* scores, int n_rows, int f, int k, int tp_rank, int tp_size,
                         int32_t* idx_global, int ld_global, int32_t* idx_local, int ld_local,
                         int32_t* counts, cudaStream_t s);

@@ -1,0 +1,138 @@
+// Shared pieces of the two persistent tcgen05 gather-GEMMs (up_proj.cu, down_proj.cu).
+//
+// CTA layout (288 threads, one CTA per SM):
+//   warps 0-3  TMA producers: each owns a quarter of every stage's B rows and
+//              issues them with tile::gather4 from one elected lane (the row ids
+//              are staged in shared memory so every TMA operand is warp-uniform);
+//              warp 0 also loads the A tile.  The full barrier of a stage expects
+//              one arrive.expect_tx per producer warp.
+//   warps 4-7  epilogue: warp 4+i reads TMEM lanes [32i, 32i+32) (= tile rows).
+//   warp 8     TMEM allocator + the single MMA-issuing thread.
+// Pipelines: kStages-deep smem ring (full/empty mbarriers) between producers
+// and MMA; two TMEM accumulators (tfull/tempty) between MMA and epilogue, so
+// the epilogue of tile i overlaps the main loop of tile i+1.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ffwd_internal.h"
+#include "sm100.cuh"
+
+namespace ffwd {
+namespace gemm {
+
+constexpr int BM = 128;            // tokens per tile (one block)
+constexpr int BK = 64;             // K per stage: 64 bf16 = one 128 B swizzle row
+constexpr int kStages = 4;
+constexpr int kProducerWarps = 4;
+constexpr int kEpiWarp0 = 4;
+constexpr int kMmaWarp = 8;
+constexpr int kThreads = 9 * 32;
+constexpr uint32_t kTmemCols = 512;
+constexpr int kABytes = BM * BK * 2;  // 16 KiB
+
+__host__ __device__ constexpr int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+struct Barriers {
+  uint64_t full[kStages];
+  uint64_t empty[kStages];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem_base;
+  uint32_t pad;
+  alignas(16) int rows[kProducerWarps][64];  // per-producer-warp gather row ids (int4 reads)
+};
+
+template <int kBBytes>
+constexpr size_t smem_bytes() {
+  return 1024 + static_cast<size_t>(kStages) * (kABytes + kBBytes) + sizeof(Barriers);
+}
+
+template <int kBBytes>
+struct Smem {
+  uint8_t* a;
+  uint8_t* b;
+  Barriers* bar;
+  __device__ explicit Smem(uint8_t* raw) {
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) &
+                                               ~uintptr_t(1023));
+    a = base;
+    b = base + kStages * kABytes;
+    bar = reinterpret_cast<Barriers*>(b + kStages * kBBytes);
+  }
+  __device__ uint8_t* a_stage(int s) const { return a + s * kABytes; }
+  __device__ uint8_t* b_stage(int s) const { return b + s * kBBytes; }
+};
+
+template <int kBBytes>
+__device__ __forceinline__ void prologue(Smem<kBBytes>& sm, int warp) {
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&sm.bar->full[i], kProducerWarps);
+      mbar_init(&sm.bar->empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.bar->tfull[i], 1);
+      mbar_init(&sm.bar->tempty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == kMmaWarp) tmem_alloc<kTmemCols>(&sm.bar->tmem_base);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+}
+
+template <int kBBytes>
+__device__ __forceinline__ void teardown(Smem<kBBytes>& sm, int warp) {
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kMmaWarp) tmem_dealloc<kTmemCols>(sm.bar->tmem_base);
+}
+
+// Neuron id at compacted position p of a block; positions past kcount map to
+// row 0 (their products land in columns that are masked or multiplied by 0).
+__device__ __forceinline__ int neuron_at(const BlockMeta& m, const int32_t* __restrict__ idx,
+                                         int ld_idx, int p) {
+  if (p >= m.kcount) return 0;
+  return m.idx_row < 0 ? p : __ldg(idx + static_cast<size_t>(m.idx_row) * ld_idx + p);
+}
+
+// Single elected thread: 4 UMMA_K=16 MMAs per stage, then release the stage.
+template <int kBBytes>
+__device__ __forceinline__ void mma_tile(Smem<kBBytes>& sm, uint32_t tmem_d, int nk,
+                                         uint32_t idesc, uint32_t b_lbo, uint32_t b_sbo,
+                                         uint32_t b_kstep, uint32_t& stage, uint32_t& phase) {
+  for (int kb = 0; kb < nk; ++kb) {
+    mbar_wait(&sm.bar->full[stage], phase);
+    tc_fence_after();
+    const uint64_t adesc = make_sdesc_sw128(smem_u32(sm.a_stage(stage)), 16, 1024);
+    const uint64_t bdesc = make_sdesc_sw128(smem_u32(sm.b_stage(stage)), b_lbo, b_sbo);
+#pragma unroll
+    for (int kk = 0; kk < BK / 16; ++kk) {
+      umma_bf16(tmem_d, adesc + static_cast<uint64_t>(2 * kk),
+                bdesc + static_cast<uint64_t>((b_kstep >> 4) * kk), idesc,
+                (kb | kk) != 0 ? 1u : 0u);
+    }
+    umma_commit(&sm.bar->empty[stage]);
+    if (++stage == kStages) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+}
+
+__device__ __forceinline__ void advance(uint32_t& stage, uint32_t& phase) {
+  if (++stage == kStages) {
+    stage = 0;
+    phase ^= 1;
+  }
+}
+
+}  // namespace gemm
+}  // namespace ffwd

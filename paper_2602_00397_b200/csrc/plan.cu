@@ -1,0 +1,140 @@
+// Device-side tile planning for the up / down gather-GEMMs.
+//
+// Reads the per-block neuron counts the top-k kernel produced (ragged under
+// tensor parallelism) and writes the block descriptors plus both persistent
+// kernels' tile tables, so no host synchronisation sits between the
+// predictor and the FFN GEMMs.
+//
+// Rasterisation: blocks are ordered dense-first, then predicted; each class
+// is cut into groups of `group` blocks, and a group's tiles are laid out
+// tile-index-major (for i: for block in group).  Concurrently running CTAs
+// therefore share the same compacted neuron window -- the selected indices
+// are ascending, so compacted tile i of every block covers about the same
+// neuron range -- while the group's X / H blocks stay L2 resident.
+#include <cuda_runtime.h>
+
+#include "ffwd_internal.h"
+
+namespace ffwd {
+
+namespace {
+
+constexpr int kPlanThreads = 512;
+constexpr int kMaxBlocks = 4096;
+constexpr int kUpBN = 256;  // rows per compensator up-projection tile
+
+__host__ __device__ constexpr int rup(int v, int m) { return (v + m - 1) / m * m; }
+
+__device__ __forceinline__ int order_to_block(int o, const PlanArgs& a) {
+  const int n_lo = a.sparse_begin;                // dense blocks before the predicted range
+  const int n_dense = a.n_blk - a.sparse_count;
+  if (o < n_lo) return o;
+  if (o < n_dense) return a.sparse_begin + a.sparse_count + (o - n_lo);
+  return a.sparse_begin + (o - n_dense);
+}
+
+__global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMeta* meta,
+                                                             Tile* up, int up_cap, Tile* down,
+                                                             int down_cap, PlanCounts* pc) {
+  __shared__ short s_nup[kMaxBlocks];   // up tiles per block, in raster order
+  __shared__ short s_ngu[kMaxBlocks];   // of which gate/up tiles
+  __shared__ int s_gbase[kMaxBlocks + 1];
+  __shared__ int s_hcols;
+  const int tid = threadIdx.x;
+  const int rc64 = rup(a.rc_local, 64);
+  if (tid == 0) s_hcols = 0;
+  __syncthreads();
+  for (int o = tid; o < a.n_blk; o += kPlanThreads) {
+    const int b = order_to_block(o, a);
+    BlockMeta m;
+    m.tok0 = b * kBlockTokens;
+    m.ntok = min(kBlockTokens, a.T - m.tok0);
+    const bool sparse = b >= a.sparse_begin && b < a.sparse_begin + a.sparse_count;
+    if (sparse) {
+      const int row = b - a.sparse_begin;
+      m.kcount = a.counts ? a.counts[row] : a.k_shared;
+      m.idx_row = a.idx_shared ? 0 : row;
+      m.comp = (a.has_comp && rc64 > 0) ? rc64 : 0;
+    } else {
+      m.kcount = a.f_local;
+      m.idx_row = -1;
+      m.comp = 0;
+    }
+    m.kpad = rup(m.kcount, 64);
+    m.ktot = m.kpad + m.comp;
+    m.n_gu = (m.kcount + 127) / 128;
+    meta[b] = m;
+    s_ngu[o] = static_cast<short>(m.n_gu);
+    s_nup[o] = static_cast<short>(m.n_gu + (m.comp + kUpBN - 1) / kUpBN);
+    atomicMax(&s_hcols, m.ktot);
+  }
+  __syncthreads();
+
+  // groups never straddle the dense / predicted boundary
+  const int n_dense = a.n_blk - a.sparse_count;
+  const int g_dense = (n_dense + a.up_group - 1) / a.up_group;
+  const int g_total = g_dense + (a.sparse_count + a.up_group - 1) / a.up_group;
+  // per-group slot counts (max tiles in the group x group size)
+  for (int g = tid; g < g_total; g += kPlanThreads) {
+    const int o0 = g < g_dense ? g * a.up_group : n_dense + (g - g_dense) * a.up_group;
+    const int o1 = min(g < g_dense ? n_dense : a.n_blk, o0 + a.up_group);
+    int mx = 0;
+    for (int o = o0; o < o1; ++o) mx = max(mx, static_cast<int>(s_nup[o]));
+    s_gbase[g + 1] = mx * (o1 - o0);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    s_gbase[0] = 0;
+    for (int g = 0; g < g_total; ++g) s_gbase[g + 1] += s_gbase[g];
+  }
+  __syncthreads();
+  const int total_up = min(s_gbase[g_total], up_cap);
+  for (int slot = tid; slot < total_up; slot += kPlanThreads) {
+    int lo = 0, hi = g_total - 1;  // last group with base <= slot
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (s_gbase[mid] <= slot) lo = mid; else hi = mid - 1;
+    }
+    const int o0 = lo < g_dense ? lo * a.up_group : n_dense + (lo - g_dense) * a.up_group;
+    const int o1 = min(lo < g_dense ? n_dense : a.n_blk, o0 + a.up_group);
+    const int sz = o1 - o0;
+    const int rel = slot - s_gbase[lo];
+    const int i = rel / sz, o = o0 + rel % sz;
+    Tile t{-1, 0, 0, 0};
+    if (i < s_ngu[o]) {
+      t = Tile{order_to_block(o, a), i * 128, 0, 0};
+    } else if (i < s_nup[o]) {
+      t = Tile{order_to_block(o, a), (i - s_ngu[o]) * kUpBN, 1, 0};
+    }
+    up[slot] = t;
+  }
+
+  // down projection: groups of down_group blocks (raster order), column-tile major
+  const int nt = a.d / a.bn_down;
+  const int total_down = min(a.n_blk * nt, down_cap);
+  for (int slot = tid; slot < total_down; slot += kPlanThreads) {
+    const int g = slot / (a.down_group * nt);
+    const int o0 = g * a.down_group;
+    const int sz = min(a.down_group, a.n_blk - o0);
+    const int rel = slot - o0 * nt;
+    const int j = rel / sz, o = o0 + rel % sz;
+    down[slot] = Tile{order_to_block(o, a), j * a.bn_down, 2, 0};
+  }
+  if (tid == 0) {
+    pc->n_up = total_up;
+    pc->n_down = total_down;
+    pc->hcols = s_hcols;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_plan(const PlanArgs& a, BlockMeta* meta, Tile* up_tiles, int up_cap,
+                        Tile* down_tiles, int down_cap, PlanCounts* counts, cudaStream_t s) {
+  if (a.n_blk > kMaxBlocks) return cudaErrorInvalidValue;
+  plan_kernel<<<1, kPlanThreads, 0, s>>>(a, meta, up_tiles, up_cap, down_tiles, down_cap,
+                                         counts);
+  return cudaGetLastError();
+}
+
+}  // namespace ffwd

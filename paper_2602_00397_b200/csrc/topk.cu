@@ -1,0 +1,182 @@
+// K1c: per-block top-k over the predictor scores (kernels.py:139-149 topk_indices,
+// sparse.py:49-55 build_mask).
+//
+// One CTA per block row.  Radix select over order-preserving 32-bit keys finds
+// the k-th largest key in four 8-bit passes (histograms in shared memory), then
+// a block-wide scan compacts the kept set in index order, so the output is
+// ascending like np.sort(argsort(-s, kind="stable")[:k]).  Ties go to the lower
+// index, -0.0 == +0.0, NaN ranks below every number (NumPy sorts NaN last).
+// Under tensor parallelism the same global selection is filtered to one rank's
+// strided shard {j : j % tp_size == tp_rank} and written as local ids j / tp_size
+// with a per-row count (the ragged per-(block, rank) k the plan kernel consumes).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ffwd_internal.h"
+
+namespace ffwd {
+
+namespace {
+
+constexpr int kTopkThreads = 1024;
+
+// Order-preserving key: larger key = earlier in np.argsort(-s, kind="stable").
+__device__ __forceinline__ uint32_t rank_key(float s) {
+  if (isnan(s)) return 0u;  // NaN sorts after every number
+  uint32_t u = __float_as_uint(s);
+  if (u == 0x80000000u) u = 0u;  // -0.0 ties with +0.0
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// Block-wide exclusive scan of one int per thread (1024 threads).
+__device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int wv = warp_tot[lane];
+    int wi = wv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    warp_tot[lane] = wi - wv;  // exclusive warp offsets
+    if (lane == 31) *total = wi;
+  }
+  __syncthreads();
+  const int r = warp_tot[warp] + incl - v;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kTopkThreads) topk_kernel(
+    const float* __restrict__ scores, int f, int k, int tp_rank, int tp_size,
+    int32_t* __restrict__ idx_global, int ld_global, int32_t* __restrict__ idx_local,
+    int ld_local, int32_t* __restrict__ counts) {
+  __shared__ int hist[256];
+  __shared__ int warp_tot[32];
+  __shared__ int s_total;
+  __shared__ uint32_t s_prefix;
+  __shared__ int s_remaining;
+  const float* s = scores + static_cast<size_t>(blockIdx.x) * f;
+  const int tid = threadIdx.x;
+
+  uint32_t prefix = 0, pmask = 0;
+  int remaining = k;
+#pragma unroll 1
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    if (tid < 256) hist[tid] = 0;
+    __syncthreads();
+    for (int i = tid; i < f; i += kTopkThreads) {
+      const uint32_t key = rank_key(s[i]);
+      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      // lane l owns bins [255-8l-7, 255-8l]; scan from the top bin down
+      int c[8], lsum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = hist[255 - 8 * tid - j];
+        lsum += c[j];
+      }
+      int incl = lsum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (tid >= o) incl += t;
+      }
+      int above = incl - lsum;  // keys in higher bins than this lane's
+      const bool mine = above < remaining && incl >= remaining;
+      if (mine) {
+        int bin = 255 - 8 * tid, cum = above;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (cum + c[j] >= remaining) {
+            bin = 255 - 8 * tid - j;
+            break;
+          }
+          cum += c[j];
+        }
+        s_prefix = prefix | (static_cast<uint32_t>(bin) << shift);
+        s_remaining = remaining - cum;
+      }
+    }
+    __syncthreads();
+    prefix = s_prefix;
+    remaining = s_remaining;
+    pmask |= 255u << shift;
+    __syncthreads();
+  }
+  const uint32_t thr = prefix;  // key of the k-th largest score
+  const int need_eq = remaining;  // how many keys == thr to keep (lowest index first)
+
+  // -- compaction in index order: contiguous chunk per thread
+  const int per = (f + kTopkThreads - 1) / kTopkThreads;
+  const int lo = min(f, tid * per), hi = min(f, lo + per);
+  int gt = 0, eq = 0;
+  for (int i = lo; i < hi; ++i) {
+    const uint32_t key = rank_key(s[i]);
+    gt += key > thr;
+    eq += key == thr;
+  }
+  const int eq_before = block_exclusive_scan(eq, warp_tot, &s_total);
+  int take_eq = min(eq, max(0, need_eq - eq_before));
+  // first pass over the chunk: count kept (global and rank-local)
+  int kept = 0, kept_loc = 0;
+  {
+    int te = take_eq;
+    for (int i = lo; i < hi; ++i) {
+      const uint32_t key = rank_key(s[i]);
+      bool keep = key > thr;
+      if (!keep && key == thr && te > 0) {
+        keep = true;
+        --te;
+      }
+      if (keep) {
+        ++kept;
+        kept_loc += (i % tp_size) == tp_rank;
+      }
+    }
+  }
+  const int pos = block_exclusive_scan(kept, warp_tot, &s_total);
+  const int pos_loc = block_exclusive_scan(kept_loc, warp_tot, &s_total);
+  if (tid == kTopkThreads - 1 && counts != nullptr) counts[blockIdx.x] = pos_loc + kept_loc;
+  int p = pos, pl = pos_loc, te = take_eq;
+  for (int i = lo; i < hi; ++i) {
+    const uint32_t key = rank_key(s[i]);
+    bool keep = key > thr;
+    if (!keep && key == thr && te > 0) {
+      keep = true;
+      --te;
+    }
+    if (!keep) continue;
+    if (idx_global) idx_global[static_cast<size_t>(blockIdx.x) * ld_global + p] = i;
+    ++p;
+    if ((i % tp_size) == tp_rank) {
+      if (idx_local) idx_local[static_cast<size_t>(blockIdx.x) * ld_local + pl] = i / tp_size;
+      ++pl;
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_topk(const float* scores, int n_rows, int f, int k, int tp_rank, int tp_size,
+                        int32_t* idx_global, int ld_global, int32_t* idx_local, int ld_local,
+                        int32_t* counts, cudaStream_t s) {
+  if (n_rows <= 0) return cudaSuccess;
+  topk_kernel<<<n_rows, kTopkThreads, 0, s>>>(scores, f, k, tp_rank, tp_size, idx_global,
+                                              ld_global, idx_local, ld_local, counts);
+  return cudaGetLastError();
+}
+
+}  // namespace ffwd

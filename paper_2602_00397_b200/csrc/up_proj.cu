@@ -1,0 +1,188 @@
+// K2: up projection of the sparse SwiGLU FFN as a tcgen05 gather-GEMM.
+//
+//   H_b[:, p] = silu(X_b . Wg[:, idx_b[p]]) * (X_b . Wu[:, idx_b[p]])   p < k_b
+//   (sparse.py:81-91: gate / up matmuls + kernels.silu, for one 128-token block b)
+//   C_b       = silu(X_b . Wc1)                                            comp tiles
+//   (compensator.py:52-58 hidden layer, predicted blocks only, engine.py:296)
+//
+// A = X_b (128 x 64 per stage) by 2-D TMA; B = the selected rows of the
+// neuron-major [gate^T | up^T | Wc1^T] (bf16, K-major) by TMA tile::gather4,
+// 128 gate + 128 up rows per gate/up tile (or 256 Wc1 rows per comp tile);
+// D = 128 x 256 f32 in TMEM; SiLU(gate) * up fused in the TMEM -> register
+// epilogue, written as bf16 into H (row stride hcols, block b at rows 128 b).
+#include "gemm_sm100.cuh"
+
+namespace ffwd {
+
+namespace {
+
+using namespace gemm;
+
+constexpr int UP_BN = 256;
+constexpr int kBBytes = UP_BN * BK * 2;  // 32 KiB per stage
+
+__global__ void __launch_bounds__(kThreads, 1)
+    up_proj_kernel(const __grid_constant__ CUtensorMap tm_x,
+                   const __grid_constant__ CUtensorMap tm_w, GemmArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  Smem<kBBytes> sm(smem_raw);
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = lane_id();
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_x);
+    tma_prefetch_desc(&tm_w);
+  }
+  prologue(sm, warp);
+  const uint32_t tmem = sm.bar->tmem_base;
+  const int n_tiles = a.counts->n_up;
+  const int nk = a.d / BK;
+
+  if (warp < kProducerWarps) {
+    // ---------------- producers: warp w gathers B rows [64w, 64w + 64) of every stage
+    const uint64_t pol_x = policy_evict_last();
+    const uint64_t pol_w = policy_evict_normal();
+    int* rows = sm.bar->rows[warp];
+    uint32_t stage = 0, phase = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const Tile tl = a.up_tiles[t];
+      if (tl.b < 0) continue;
+      const BlockMeta m = a.meta[tl.b];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = 64 * warp + 32 * h + static_cast<int>(lane);  // B row within the tile
+        int r;
+        if (tl.kind == 0) {
+          const int half = j >> 7;  // 0 = gate rows, 1 = up rows
+          r = neuron_at(m, a.idx, a.ld_idx, tl.n0 + (j & 127)) + half * a.f_local;
+        } else {
+          r = 2 * a.f_local + tl.n0 + j;
+        }
+        rows[32 * h + lane] = r;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t bytes = 64 * BK * 2 + (warp == 0 ? kABytes : 0);
+        const int4* rq = reinterpret_cast<const int4*>(rows);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&sm.bar->empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&sm.bar->full[stage], bytes);
+          if (warp == 0)
+            tma_load_2d(&tm_x, &sm.bar->full[stage], sm.a_stage(stage), kb * BK, m.tok0, pol_x);
+          uint8_t* dst = sm.b_stage(stage) + warp * 64 * 128;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int4 r = rq[q];
+            tma_gather4(&tm_w, &sm.bar->full[stage], dst + q * 512, kb * BK, r.x, r.y, r.z, r.w,
+                        pol_w);
+          }
+          advance(stage, phase);
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp == kMmaWarp) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = make_idesc_bf16(BM, UP_BN, false, false);
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const Tile tl = a.up_tiles[t];
+        if (tl.b < 0) continue;
+        mbar_wait_sleep(&sm.bar->tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        mma_tile(sm, tmem + acc * UP_BN, nk, idesc, 16, 1024, 32, stage, phase);
+        umma_commit(&sm.bar->tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue: TMEM -> regs -> SiLU(g) * u -> bf16 H
+    const int ew = warp - kEpiWarp0;
+    const int row = ew * 32 + static_cast<int>(lane);
+    uint32_t acc = 0, acc_phase = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const Tile tl = a.up_tiles[t];
+      if (tl.b < 0) continue;
+      const BlockMeta m = a.meta[tl.b];
+      mbar_wait_sleep(&sm.bar->tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tb = tmem + acc * UP_BN + (static_cast<uint32_t>(ew * 32) << 16);
+      __nv_bfloat16* hrow = static_cast<__nv_bfloat16*>(a.h) +
+                            static_cast<size_t>(tl.b * kBlockTokens + row) * a.hcols;
+      if (tl.kind == 0) {
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+          const int pos = tl.n0 + c;
+          if (pos >= m.kpad) break;
+          uint32_t g[32], u[32];
+          tmem_ld32(tb + c, g);
+          tmem_ld32(tb + 128 + c, u);
+          tmem_ld_wait();
+          uint32_t packed[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float h0 = silu_f32(__uint_as_float(g[2 * j])) * __uint_as_float(u[2 * j]);
+            float h1 = silu_f32(__uint_as_float(g[2 * j + 1])) * __uint_as_float(u[2 * j + 1]);
+            if (pos + 2 * j >= m.kcount) h0 = 0.0f;
+            if (pos + 2 * j + 1 >= m.kcount) h1 = 0.0f;
+            packed[j] = pack_bf16x2(h0, h1);
+          }
+          uint4* dst = reinterpret_cast<uint4*>(hrow + pos);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2],
+                                packed[4 * j + 3]);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < UP_BN; c += 32) {
+          const int col = tl.n0 + c;
+          if (col >= m.comp) break;
+          uint32_t g[32];
+          tmem_ld32(tb + c, g);
+          tmem_ld_wait();
+          uint32_t packed[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            packed[j] = pack_bf16x2(silu_f32(__uint_as_float(g[2 * j])),
+                                    silu_f32(__uint_as_float(g[2 * j + 1])));
+          uint4* dst = reinterpret_cast<uint4*>(hrow + m.kpad + col);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2],
+                                packed[4 * j + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&sm.bar->tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+  teardown(sm, warp);
+}
+
+}  // namespace
+
+cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s) {
+  CUtensorMap tx, tw;
+  if (encode_tmap_2d_bf16(&tx, a.x, a.d, a.T, BK, BM) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  if (encode_tmap_2d_bf16(&tw, a.wgu_t, a.d, a.wgu_rows, BK, 1) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  constexpr size_t smem = smem_bytes<kBBytes>();
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e =
+        cudaFuncSetAttribute(up_proj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int grid = a.num_sms < a.up_cap ? a.num_sms : a.up_cap;
+  up_proj_kernel<<<grid, kThreads, smem, s>>>(tx, tw, a);
+  return cudaGetLastError();
+}
+
+}  // namespace ffwd

@@ -106,7 +106,7 @@ def predictor_scores(dp: DevicePredictor, x: torch.Tensor, blk_begin: int = 0,
         blk_count = n_blk - blk_begin
     lib = _dev.lib_for(x.device)
     scores = torch.empty((blk_count, dp.f), dtype=torch.float32, device=x.device)
-    ws_n = lib.ffwd_predictor_workspace_bytes(blk_count, dp.d, dp.r)
+    ws_n = lib.ffwd_predictor_workspace_bytes(blk_count, dp.d, dp.r, dp.f)
     ws = _dev.workspace(x.device, ws_n)
     _lib.check(lib.ffwd_predictor_forward(
         x.data_ptr(), int(x.dtype == torch.float32), T, dp.d, blk_begin, blk_count,
