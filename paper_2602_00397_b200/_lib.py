@@ -13,7 +13,7 @@ import threading
 from .errors import UnsupportedError, ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libffwd_b200.so")
+LIB_PATH = os.environ.get("FFWD_LIB") or os.path.join(_HERE, "libffwd_b200.so")
 
 FFWD_OK, FFWD_ERR_VALIDATION, FFWD_ERR_CUDA, FFWD_ERR_UNSUPPORTED = 0, 1, 2, 3
 

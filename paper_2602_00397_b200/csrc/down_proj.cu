@@ -38,26 +38,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int n_tiles = a.counts->n_down;
 
   if (warp < kProducerWarps) {
-    // ---------------- producers: warp w gathers K rows [16w, 16w + 16) of every stage
+    // ---------------- producers: warp w gathers K rows [Q w, Q w + Q) of every stage
+    constexpr int Q = BK / kProducerWarps;  // K rows per producer warp (multiple of 4)
     const uint64_t pol_h = policy_evict_last();
     const uint64_t pol_w = policy_evict_normal();
     int* rows = sm.bar->rows[warp];
     uint32_t stage = 0, phase = 0;
-    const uint32_t bytes = 16 * BN * 2 + (warp == 0 ? kABytes : 0);
+    const uint32_t bytes = Q * BN * 2 + (warp == 0 ? kABytes : 0);
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
       const Tile tl = a.down_tiles[t];
       if (tl.b < 0) continue;
       const BlockMeta m = a.meta[tl.b];
       const int nk = m.ktot / BK;
       auto row_of = [&](int kb) -> int {
-        const int p = kb * BK + 16 * warp + static_cast<int>(lane & 15);
+        const int p = kb * BK + Q * warp + static_cast<int>(lane % Q);
         return p < m.kpad ? neuron_at(m, a.idx, a.ld_idx, p) : a.f_local + (p - m.kpad);
       };
       int next = row_of(0);
       for (int kb = 0; kb < nk; ++kb) {
         const int cur = next;
         if (kb + 1 < nk) next = row_of(kb + 1);  // prefetch: consumed next iteration
-        if (lane < 16) rows[lane] = cur;
+        if (lane < Q) rows[lane] = cur;
         __syncwarp();
         if (lane == 0) {
           mbar_wait(&sm.bar->empty[stage], phase ^ 1);
@@ -66,15 +67,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_2d(&tm_h, &sm.bar->full[stage], sm.a_stage(stage), kb * BK,
                         tl.b * kBlockTokens, pol_h);
           const int4* rq = reinterpret_cast<const int4*>(rows);
-          uint8_t* dst = sm.b_stage(stage) + warp * 2 * 1024;  // K rows 16w.. = 2 atoms
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < Q / 4; ++q) {
             const int4 r = rq[q];
+            const int pos = Q * warp + 4 * q;  // K row within the stage
+            uint8_t* dst = sm.b_stage(stage) + (pos >> 3) * 1024 + (pos & 7) * 128;
 #pragma unroll
             for (int c = 0; c < kChunks; ++c)
-              tma_gather4(&tm_w, &sm.bar->full[stage],
-                          dst + c * kLbo + (q >> 1) * 1024 + (q & 1) * 512, tl.n0 + c * 64, r.x,
-                          r.y, r.z, r.w, pol_w);
+              tma_gather4(&tm_w, &sm.bar->full[stage], dst + c * kLbo, tl.n0 + c * 64, r.x, r.y,
+                          r.z, r.w, pol_w);
           }
         }
         __syncwarp();

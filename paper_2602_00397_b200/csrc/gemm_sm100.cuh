@@ -1,13 +1,14 @@
 // Shared pieces of the two persistent tcgen05 gather-GEMMs (up_proj.cu, down_proj.cu).
 //
-// CTA layout (288 threads, one CTA per SM):
-//   warps 0-3  TMA producers: each owns a quarter of every stage's B rows and
-//              issues them with tile::gather4 from one elected lane (the row ids
-//              are staged in shared memory so every TMA operand is warp-uniform);
-//              warp 0 also loads the A tile.  The full barrier of a stage expects
-//              one arrive.expect_tx per producer warp.
-//   warps 4-7  epilogue: warp 4+i reads TMEM lanes [32i, 32i+32) (= tile rows).
-//   warp 8     TMEM allocator + the single MMA-issuing thread.
+// CTA layout (P = kProducerWarps, one CTA per SM):
+//   warps 0..P-1   TMA producers: each owns 1/P of every stage's B rows and issues
+//                  them with tile::gather4 from one lane (row ids staged in shared
+//                  memory so every TMA operand is warp-uniform); warp 0 also loads
+//                  the A tile.  gather4 throughput is set by the number of issuing
+//                  warps (tools/tma_bench.cu), hence several producer warps.  The
+//                  full barrier of a stage expects one arrive.expect_tx per warp.
+//   warps P..P+3   epilogue: warp P+i reads TMEM lanes [32i, 32i+32) (tile rows).
+//   warp P+4       TMEM allocator + the single MMA-issuing thread.
 // Pipelines: kStages-deep smem ring (full/empty mbarriers) between producers
 // and MMA; two TMEM accumulators (tfull/tempty) between MMA and epilogue, so
 // the epilogue of tile i overlaps the main loop of tile i+1.
@@ -28,10 +29,14 @@ namespace gemm {
 constexpr int BM = 128;            // tokens per tile (one block)
 constexpr int BK = 64;             // K per stage: 64 bf16 = one 128 B swizzle row
 constexpr int kStages = 4;
-constexpr int kProducerWarps = 4;
-constexpr int kEpiWarp0 = 4;
-constexpr int kMmaWarp = 8;
-constexpr int kThreads = 9 * 32;
+#ifndef FFWD_PRODUCER_WARPS
+#define FFWD_PRODUCER_WARPS 8
+#endif
+constexpr int kProducerWarps = FFWD_PRODUCER_WARPS;  // TMA gather4 issue rate scales with warps
+constexpr int kEpiWarp0 = kProducerWarps;            // multiple of 4: warp % 4 = TMEM lane quadrant
+constexpr int kMmaWarp = kProducerWarps + 4;
+constexpr int kThreads = (kProducerWarps + 5) * 32;
+static_assert(kProducerWarps % 4 == 0 && 64 % kProducerWarps == 0, "producer split");
 constexpr uint32_t kTmemCols = 512;
 constexpr int kABytes = BM * BK * 2;  // 16 KiB
 
@@ -44,7 +49,7 @@ struct Barriers {
   uint64_t tempty[2];
   uint32_t tmem_base;
   uint32_t pad;
-  alignas(16) int rows[kProducerWarps][64];  // per-producer-warp gather row ids (int4 reads)
+  alignas(16) int rows[kProducerWarps][256 / kProducerWarps];  // gather row ids (int4 reads)
 };
 
 template <int kBBytes>

@@ -38,7 +38,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nk = a.d / BK;
 
   if (warp < kProducerWarps) {
-    // ---------------- producers: warp w gathers B rows [64w, 64w + 64) of every stage
+    // ---------------- producers: warp w gathers B rows [R w, R w + R) of every stage
+    constexpr int R = UP_BN / kProducerWarps;  // rows per producer warp
     const uint64_t pol_x = policy_evict_last();
     const uint64_t pol_w = policy_evict_normal();
     int* rows = sm.bar->rows[warp];
@@ -47,9 +48,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Tile tl = a.up_tiles[t];
       if (tl.b < 0) continue;
       const BlockMeta m = a.meta[tl.b];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int j = 64 * warp + 32 * h + static_cast<int>(lane);  // B row within the tile
+      for (int i = static_cast<int>(lane); i < R; i += 32) {
+        const int j = R * warp + i;  // B row within the tile
         int r;
         if (tl.kind == 0) {
           const int half = j >> 7;  // 0 = gate rows, 1 = up rows
@@ -57,20 +57,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
           r = 2 * a.f_local + tl.n0 + j;
         }
-        rows[32 * h + lane] = r;
+        rows[i] = r;
       }
       __syncwarp();
       if (lane == 0) {
-        const uint32_t bytes = 64 * BK * 2 + (warp == 0 ? kABytes : 0);
+        const uint32_t bytes = R * BK * 2 + (warp == 0 ? kABytes : 0);
         const int4* rq = reinterpret_cast<const int4*>(rows);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&sm.bar->empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&sm.bar->full[stage], bytes);
           if (warp == 0)
             tma_load_2d(&tm_x, &sm.bar->full[stage], sm.a_stage(stage), kb * BK, m.tok0, pol_x);
-          uint8_t* dst = sm.b_stage(stage) + warp * 64 * 128;
+          uint8_t* dst = sm.b_stage(stage) + warp * R * 128;
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
+          for (int q = 0; q < R / 4; ++q) {
             const int4 r = rq[q];
             tma_gather4(&tm_w, &sm.bar->full[stage], dst + q * 512, kb * BK, r.x, r.y, r.z, r.w,
                         pol_w);

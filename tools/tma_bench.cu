@@ -1,0 +1,228 @@
+// Microbenchmark: TMA 2-D tile loads vs tile::gather4 into shared memory (no MMA).
+// Measures L2->SMEM delivery rate per SM for the access patterns of the up/down
+// gather-GEMMs.  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17
+//   -I../paper_2602_00397_b200/csrc tma_bench.cu -o tma_bench
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include <algorithm>
+
+#include "sm100.cuh"
+
+using namespace ffwd;
+
+constexpr int kMaxStages = 6;
+constexpr int kStageBytes = 32768;
+
+struct Bars {
+  uint64_t full[kMaxStages];
+};
+
+// mode 0: one 2-D tile (64 x 256 rows) per stage; mode 1: 64 gather4 (256 rows) per
+// stage issued by one thread; mode 2: 64 gather4 issued by 4 warps (16 each).
+__global__ void __launch_bounds__(512, 1)
+    tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_constant__ CUtensorMap tm_g,
+               const int* __restrict__ rows_all, int n_rowsets, int iters, int stages, int mode,
+               int kdim, unsigned long long* cycles, const __nv_bfloat16* wptr) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  Bars* bars = reinterpret_cast<Bars*>(base + kMaxStages * kStageBytes);
+  __shared__ int srows[256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // barrier arrivals per fill: TMA modes count issuing warps; cp.async modes count threads
+  const int nwarps_issue = mode == 7 ? 128 : mode == 8 ? 256 : mode == 9 ? 128 + 2 :
+                           mode == 5 ? 8 : (mode == 6 ? 16 : (mode >= 2 ? 4 : 1));
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kMaxStages; ++i) mbar_init(&bars->full[i], nwarps_issue);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int* rows = rows_all + (blockIdx.x % n_rowsets) * 256;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) srows[i] = rows[i];
+  __syncthreads();
+  const uint64_t pol = policy_evict_normal();
+  unsigned long long t0 = clock64();
+  uint32_t phase_bits = 0;
+  const int nk = kdim / 64;
+  for (int it = 0; it < iters; ++it) {
+    const int s = it % stages;
+    if (it >= stages) {  // wait for the stage's previous fill
+      if (threadIdx.x == 0 || (mode == 2 && lane == 0 && warp < 4)) {
+      }
+      mbar_wait_sleep(&bars->full[s], (phase_bits >> s) & 1, 2000);
+      phase_bits ^= 1u << s;
+    }
+    __syncthreads();
+    const int kb = (it + blockIdx.x) % nk;
+    uint8_t* dst = base + s * kStageBytes;
+    if (mode == 0) {
+      if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&bars->full[s], kStageBytes);
+        tma_load_2d(&tm_tile, &bars->full[s], dst, kb * 64, (blockIdx.x * 256) % 16384, pol);
+      }
+    } else if (mode == 1) {
+      if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(&bars->full[s], kStageBytes);
+        const int4* rq = reinterpret_cast<const int4*>(srows);
+        for (int q = 0; q < 64; ++q) {
+          const int4 r = rq[q];
+          tma_gather4(&tm_g, &bars->full[s], dst + q * 512, kb * 64, r.x, r.y, r.z, r.w, pol);
+        }
+      }
+    } else if (mode == 2) {
+      if (warp < 4 && lane == 0) {
+        mbar_arrive_expect_tx(&bars->full[s], kStageBytes / 4);
+        const int4* rq = reinterpret_cast<const int4*>(srows) + warp * 16;
+        for (int q = 0; q < 16; ++q) {
+          const int4 r = rq[q];
+          tma_gather4(&tm_g, &bars->full[s], dst + (warp * 16 + q) * 512, kb * 64, r.x, r.y, r.z,
+                      r.w, pol);
+        }
+      }
+    } else if (mode == 3) {  // 4 warps, rows preloaded, fully unrolled issue
+      if (warp < 4 && lane == 0) {
+        mbar_arrive_expect_tx(&bars->full[s], kStageBytes / 4);
+        const int4* rq = reinterpret_cast<const int4*>(srows) + warp * 16;
+        int4 r[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) r[q] = rq[q];
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          tma_gather4(&tm_g, &bars->full[s], dst + (warp * 16 + q) * 512, kb * 64, r[q].x,
+                      r[q].y, r[q].z, r[q].w, pol);
+      }
+    } else if (mode >= 7) {  // cp.async 16 B per thread (LDGSTS), swizzled like TMA
+      const int nthr = mode == 7 ? 128 : (mode == 8 ? 256 : 128);
+      const int rows_cp = mode == 9 ? 128 : 256;  // mode 9: half the rows via cp.async
+      const int row0 = mode == 9 ? 128 : 0;
+      if (mode == 9 && (warp == 4 || warp == 5) && lane == 0) {  // 2 warps: 32 gather4
+        mbar_arrive_expect_tx(&bars->full[s], kStageBytes / 4);
+        const int4* rq = reinterpret_cast<const int4*>(srows) + (warp - 4) * 16;
+        for (int q = 0; q < 16; ++q) {
+          const int4 r = rq[q];
+          tma_gather4(&tm_g, &bars->full[s], dst + ((warp - 4) * 16 + q) * 512, kb * 64, r.x,
+                      r.y, r.z, r.w, pol);
+        }
+      }
+      if (threadIdx.x < nthr) {
+        const int c = threadIdx.x & 7;
+        for (int rr = threadIdx.x >> 3; rr < rows_cp; rr += nthr >> 3) {
+          const int row = row0 + rr;
+          const __nv_bfloat16* src = wptr + static_cast<size_t>(srows[row]) * kdim + kb * 64 + c * 8;
+          const uint32_t d = smem_u32(dst + row * 128 + ((c ^ (row & 7)) << 4));
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars->full[s])) : "memory");
+      }
+    } else if (mode >= 5) {  // 8 or 16 issuing warps
+      const int nw = mode == 5 ? 8 : 16, per = 64 / nw;
+      if (warp < nw && lane == 0) {
+        mbar_arrive_expect_tx(&bars->full[s], kStageBytes / nw);
+        const int4* rq = reinterpret_cast<const int4*>(srows) + warp * per;
+        for (int q = 0; q < per; ++q) {
+          const int4 r = rq[q];
+          tma_gather4(&tm_g, &bars->full[s], dst + (warp * per + q) * 512, kb * 64, r.x, r.y,
+                      r.z, r.w, pol);
+        }
+      }
+    } else {  // mode 4: all 4 warps, each lane issues 0.5 gather4 (lanes 0..15), waterfall
+      if (warp < 4) {
+        if (lane == 0) mbar_arrive_expect_tx(&bars->full[s], kStageBytes / 4);
+        __syncwarp();
+        if (lane < 16) {
+          const int4 r = reinterpret_cast<const int4*>(srows)[warp * 16 + lane];
+          tma_gather4(&tm_g, &bars->full[s], dst + (warp * 16 + lane) * 512, kb * 64, r.x, r.y,
+                      r.z, r.w, pol);
+        }
+      }
+    }
+  }
+  // drain
+  for (int i = 0; i < stages && i < iters; ++i) {
+    const int it = iters - stages + i;
+    if (it < 0) continue;
+    const int s = it % stages;
+    mbar_wait_sleep(&bars->full[s], (phase_bits >> s) & 1, 2000);
+    phase_bits ^= 1u << s;
+  }
+  unsigned long long t1 = clock64();
+  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+int main(int argc, char** argv) {
+  const int rows_total = 16384, kdim = 4096;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  EncodeFn enc = reinterpret_cast<EncodeFn>(fn);
+  void* w;
+  cudaMalloc(&w, size_t(rows_total) * kdim * 2);
+  cudaMemset(w, 0, size_t(rows_total) * kdim * 2);
+  CUtensorMap tile, g;
+  cuuint64_t dims[2] = {cuuint64_t(kdim), cuuint64_t(rows_total)};
+  cuuint64_t str[1] = {cuuint64_t(kdim) * 2};
+  cuuint32_t box_t[2] = {64, 256}, box_g[2] = {64, 1}, es[2] = {1, 1};
+  enc(&tile, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box_t, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const int promo = argc > 2 ? atoi(argv[2]) : 3;  // 0 none, 1 64B, 2 128B, 3 256B
+  enc(&g, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box_g, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_128B, (CUtensorMapL2promotion)promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  printf("gather promotion %d\n", promo);
+  const int n_sets = 148;
+  std::vector<int> hrows(n_sets * 256);
+  srand(1);
+  const int span = argc > 1 ? atoi(argv[1]) : 2048;  // row window the gathered rows come from
+  for (int s = 0; s < n_sets; ++s) {
+    int lo = span < rows_total ? (s * 97) % (rows_total - span) : 0;
+    std::vector<int> pick;
+    for (int i = 0; i < 256; ++i) pick.push_back(lo + (rand() % span));
+    std::sort(pick.begin(), pick.end());
+    for (int i = 0; i < 256; ++i) hrows[s * 256 + i] = pick[i];
+  }
+  int* drows;
+  cudaMalloc(&drows, hrows.size() * 4);
+  cudaMemcpy(drows, hrows.data(), hrows.size() * 4, cudaMemcpyHostToDevice);
+  unsigned long long* dcyc;
+  cudaMalloc(&dcyc, 148 * 8);
+  const size_t smem = 1024 + kMaxStages * kStageBytes + sizeof(Bars);
+  cudaFuncSetAttribute(tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int iters = 2000;
+  const char* names[10] = {"tile 64x256", "gather4 x64 (1 thread)", "gather4 x64 (4 warps)",
+                          "gather4 4w preload", "gather4 4w x16 lanes", "gather4 8 warps",
+                          "gather4 16 warps", "cp.async 128 thr", "cp.async 256 thr",
+                          "half gather4 + half cp.async"};
+  for (int mode = 0; mode < 10; ++mode) {
+    if (mode == 1 || mode == 3 || mode == 4 || mode == 7 || mode == 9) continue;
+    for (int stages : {4}) {
+      tma_kernel<<<148, 512, smem>>>(tile, g, drows, n_sets, 50, stages, mode, kdim, dcyc, (const __nv_bfloat16*)w);
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0);
+      tma_kernel<<<148, 512, smem>>>(tile, g, drows, n_sets, iters, stages, mode, kdim, dcyc, (const __nv_bfloat16*)w);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      std::vector<unsigned long long> c(148);
+      cudaMemcpy(c.data(), dcyc, 148 * 8, cudaMemcpyDeviceToHost);
+      double avg = 0;
+      for (auto v : c) avg += v;
+      avg /= 148;
+      const double bytes = 148.0 * iters * kStageBytes;
+      printf("%-24s stages=%d span=%d: %.1f cyc/stage/SM, %.2f TB/s aggregate (%.3f ms) %s\n",
+             names[mode], stages, span, avg / iters, bytes / (ms * 1e-3) / 1e12, ms,
+             cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  return 0;
+}
