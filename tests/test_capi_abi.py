@@ -1,0 +1,80 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports and binds
+every entry point include/ffwd_b200.h declares, host-only entry points work,
+and compute entry points fail loudly (no CPU fallback) when there is no GPU."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2602_00397_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ffwd_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"FFWD_API\s+[\w\s\*]+?\b(ffwd_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    assert {"ffwd_ffn_layer", "ffwd_predictor_forward", "ffwd_topk", "ffwd_sparse_ffn",
+            "ffwd_predict_topk", "ffwd_layer_workspace_bytes"} <= set(syms)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load_library()
+    for name in declared_symbols():
+        assert hasattr(lib, name), f"{name} declared in the header but not exported"
+        assert name in _lib.SIGNATURES, f"{name} not bound in _lib.SIGNATURES"
+    assert set(_lib.SIGNATURES) == set(declared_symbols())
+
+
+def test_abi_version_and_host_only_calls():
+    lib = _lib.load_library()
+    assert lib.ffwd_abi_version() == 1
+    # workspace sizing is pure host arithmetic
+    ws = lib.ffwd_layer_workspace_bytes(16384, 4096, 14336, 14336, 512, 256, 7168, 1, 1)
+    h_bytes = 128 * 128 * 14336 * 2  # H for 128 blocks at the dense width
+    assert h_bytes < ws < h_bytes + 64 * 2 ** 20
+    assert lib.ffwd_predictor_workspace_bytes(126, 4096, 256, 14336) > 126 * 4096 * 4
+    assert lib.ffwd_sparse_ffn_workspace_bytes(1024, 512, 1376, 64, 688) > 0
+    assert lib.ffwd_set_raster(32, 8) == _lib.FFWD_OK
+    assert lib.ffwd_set_raster(0, 8) == _lib.FFWD_ERR_VALIDATION
+    assert b"raster" in lib.ffwd_last_error()
+    for i in range(7):
+        assert lib.ffwd_stage_name(i)
+
+
+def test_validation_happens_before_any_launch():
+    lib = _lib.load_library()
+    # k out of range -> FFWD_ERR_VALIDATION (ValidationError), no device touched
+    rc = lib.ffwd_topk(None, 1, 10, 11, 0, 1, None, 0, None, 0, None, None)
+    assert rc == _lib.FFWD_ERR_VALIDATION
+    with pytest.raises(_lib.ValidationError):
+        _lib.check(rc, "topk")
+    rc = lib.ffwd_topk(None, 1, 10, 5, 3, 2, None, 0, None, 0, None, None)
+    assert rc == _lib.FFWD_ERR_VALIDATION and b"rank" in lib.ffwd_last_error()
+    rc = lib.ffwd_ffn_layer(None, 256, 96, None, None, 200, 12, None, None, None, 8, 200, 100, 1,
+                            1, 0, 1, None, None, None, None, 0, None, 0, None)
+    assert rc == _lib.FFWD_ERR_UNSUPPORTED  # d_model % 64 != 0
+    with pytest.raises(_lib.UnsupportedError):
+        _lib.check(rc, "ffn_layer")
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU path")
+def test_compute_path_fails_loudly_without_gpu():
+    import paper_2602_00397_b200 as ff
+    from oracle import ffwd_oracle as orc
+    pred = orc.init_predictor(np.random.default_rng(0), 64, 200)
+    x = np.ones((8, 64), np.float32)
+    with pytest.raises(RuntimeError):
+        ff.predictor_forward(ff.PredictorParams(**pred), x)
+    with pytest.raises(RuntimeError):
+        ff.topk_indices(np.ones(4, np.float32), 2)
+    with pytest.raises(RuntimeError):
+        _lib.require_device(0)
