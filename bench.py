@@ -274,6 +274,8 @@ def run_gpu(args, rank: int, world: int) -> None:
     from paper_2602_00397_b200 import layer as fl
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
+    if args.raster:
+        fl.set_raster(*(int(v) for v in args.raster.split(",")))
     peaks = load_peaks()
     d, f, L, T, keep = CONFIGS[args.config]
     if args.layers:
@@ -445,6 +447,7 @@ def main():
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug)")
     ap.add_argument("--skip-dense", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--raster", default="", help="UP,DOWN blocks per L2 raster group (tuning)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -10,6 +10,10 @@
 // contiguous = MN-major) by TMA tile::gather4 in BN/64 column atoms; D = 128 x BN
 // f32 in TMEM.  Epilogue: optional residual add (engine.py:308) and optional
 // bf16 copy for the next layer's input, f32 Y stores.
+// 8 issuing warps (r1 A/B: 16 warps gave no gain here: 1.07 vs 1.09 ms/layer).
+#ifndef FFWD_PRODUCER_WARPS
+#define FFWD_PRODUCER_WARPS 8
+#endif
 #include "gemm_sm100.cuh"
 
 namespace ffwd {
@@ -21,7 +25,8 @@ using namespace gemm;
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     down_proj_kernel(const __grid_constant__ CUtensorMap tm_h,
-                     const __grid_constant__ CUtensorMap tm_w, GemmArgs a) {
+                     const __grid_constant__ CUtensorMap tm_w,
+                     const __grid_constant__ CUtensorMap tm_wt, GemmArgs a) {
   constexpr int kBBytes = BK * BN * 2;
   constexpr int kChunks = BN / 64;            // 64-column (128 B) atoms along N
   constexpr uint32_t kLbo = (BK / 8) * 1024;  // MN-direction atom stride
@@ -32,6 +37,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_h);
     tma_prefetch_desc(&tm_w);
+    tma_prefetch_desc(&tm_wt);
   }
   prologue(sm, warp);
   const uint32_t tmem = sm.bar->tmem_base;
@@ -44,7 +50,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t pol_w = policy_evict_normal();
     int* rows = sm.bar->rows[warp];
     uint32_t stage = 0, phase = 0;
-    const uint32_t bytes = Q * BN * 2 + (warp == 0 ? kABytes : 0);
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
       const Tile tl = a.down_tiles[t];
       if (tl.b < 0) continue;
@@ -58,24 +63,42 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < nk; ++kb) {
         const int cur = next;
         if (kb + 1 < nk) next = row_of(kb + 1);  // prefetch: consumed next iteration
+        // Contiguous K rows (identity index of dense blocks, compensator rows past kpad)
+        // take the 2-D tile path: one 64-row box per column atom, issued by warp 0.
+        const bool contiguous = m.idx_row < 0 || kb * BK >= m.kpad;
         if (lane < Q) rows[lane] = cur;
         __syncwarp();
         if (lane == 0) {
           mbar_wait(&sm.bar->empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&sm.bar->full[stage], bytes);
-          if (warp == 0)
+          uint32_t nbytes = contiguous ? 0 : Q * BN * 2;
+          if (warp == 0) nbytes += kABytes + (contiguous ? BK * BN * 2 : 0);
+          if (nbytes)
+            mbar_arrive_expect_tx(&sm.bar->full[stage], nbytes);
+          else
+            mbar_arrive(&sm.bar->full[stage]);
+          if (warp == 0) {
             tma_load_2d(&tm_h, &sm.bar->full[stage], sm.a_stage(stage), kb * BK,
                         tl.b * kBlockTokens, pol_h);
-          const int4* rq = reinterpret_cast<const int4*>(rows);
+            if (contiguous) {
+              const int r0 = m.idx_row < 0 ? kb * BK : a.f_local + (kb * BK - m.kpad);
 #pragma unroll
-          for (int q = 0; q < Q / 4; ++q) {
-            const int4 r = rq[q];
-            const int pos = Q * warp + 4 * q;  // K row within the stage
-            uint8_t* dst = sm.b_stage(stage) + (pos >> 3) * 1024 + (pos & 7) * 128;
+              for (int c = 0; c < kChunks; ++c)
+                tma_load_2d(&tm_wt, &sm.bar->full[stage], sm.b_stage(stage) + c * kLbo,
+                            tl.n0 + c * 64, r0, pol_w);
+            }
+          }
+          if (!contiguous) {
+            const int4* rq = reinterpret_cast<const int4*>(rows);
 #pragma unroll
-            for (int c = 0; c < kChunks; ++c)
-              tma_gather4(&tm_w, &sm.bar->full[stage], dst + c * kLbo, tl.n0 + c * 64, r.x, r.y,
-                          r.z, r.w, pol_w);
+            for (int q = 0; q < Q / 4; ++q) {
+              const int4 r = rq[q];
+              const int pos = Q * warp + 4 * q;  // K row within the stage
+              uint8_t* dst = sm.b_stage(stage) + (pos >> 3) * 1024 + (pos & 7) * 128;
+#pragma unroll
+              for (int c = 0; c < kChunks; ++c)
+                tma_gather4(&tm_w, &sm.bar->full[stage], dst + c * kLbo, tl.n0 + c * 64, r.x,
+                            r.y, r.z, r.w, pol_w);
+            }
           }
         }
         __syncwarp();
@@ -114,18 +137,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const size_t row_off = static_cast<size_t>(m.tok0 + row) * a.d + tl.n0;
       const bool live = row < m.ntok;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t v[32];
-        tmem_ld32(tb + c, v);
+      for (int c = 0; c < BN; c += 16) {
+        uint32_t v[16];
+        tmem_ld16(tb + c, v);
         tmem_ld_wait();
         if (live) {
-          float o[32];
+          float o[16];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) o[j] = __uint_as_float(v[j]);
+          for (int j = 0; j < 16; ++j) o[j] = __uint_as_float(v[j]);
           if (a.residual) {  // fused residual add (engine.py:308)
             const float4* res = reinterpret_cast<const float4*>(a.residual + row_off + c);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < 4; ++j) {
               const float4 r = res[j];
               o[4 * j] += r.x;
               o[4 * j + 1] += r.y;
@@ -135,13 +158,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           float4* dst = reinterpret_cast<float4*>(a.y + row_off + c);
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
+          for (int j = 0; j < 4; ++j)
             dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
           if (a.x_next) {  // next layer's bf16 input
             uint4* xn = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.x_next) +
                                                  row_off + c);
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < 2; ++j)
               xn[j] = make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]),
                                  pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
                                  pack_bf16x2(o[8 * j + 4], o[8 * j + 5]),
@@ -160,11 +183,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int BN>
 cudaError_t launch_bn(const GemmArgs& a, cudaStream_t s) {
-  CUtensorMap th, tw;
+  CUtensorMap th, tw, twt;
   if (encode_tmap_2d_bf16(&th, a.h, a.hcols, static_cast<uint64_t>(a.n_blk) * BM, BK, BM) !=
       CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   if (encode_tmap_2d_bf16(&tw, a.wd, a.d, a.wd_rows, 64, 1) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  if (encode_tmap_2d_bf16(&twt, a.wd, a.d, a.wd_rows, 64, BK) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   constexpr size_t smem = smem_bytes<BK * BN * 2>();
   static bool attr = false;
@@ -175,7 +200,7 @@ cudaError_t launch_bn(const GemmArgs& a, cudaStream_t s) {
     attr = true;
   }
   const int grid = a.num_sms < a.down_cap ? a.num_sms : a.down_cap;
-  down_proj_kernel<BN><<<grid, kThreads, smem, s>>>(th, tw, a);
+  down_proj_kernel<BN><<<grid, kThreads, smem, s>>>(th, tw, twt, a);
   return cudaGetLastError();
 }
 

@@ -25,8 +25,11 @@
 
 namespace ffwd {
 namespace gemm {
+// Each kernel TU picks its own producer-warp count (FFWD_PRODUCER_WARPS before the
+// include), so everything here has internal linkage.
+namespace {
 
-constexpr int BM = 128;            // tokens per tile (one block)
+constexpr int BM = 128;           // tokens per tile (one block)
 constexpr int BK = 64;             // K per stage: 64 bf16 = one 128 B swizzle row
 constexpr int kStages = 4;
 #ifndef FFWD_PRODUCER_WARPS
@@ -139,5 +142,6 @@ __device__ __forceinline__ void advance(uint32_t& stage, uint32_t& phase) {
   }
 }
 
+}  // namespace
 }  // namespace gemm
 }  // namespace ffwd

@@ -10,6 +10,11 @@
 // 128 gate + 128 up rows per gate/up tile (or 256 Wc1 rows per comp tile);
 // D = 128 x 256 f32 in TMEM; SiLU(gate) * up fused in the TMEM -> register
 // epilogue, written as bf16 into H (row stride hcols, block b at rows 128 b).
+// 16 issuing warps: gathers here are 128 B rows at 8 KiB stride, the up projection is
+// gather-rate bound (r1 A/B: 2.39 -> 2.21 ms/layer vs 8 warps).
+#ifndef FFWD_PRODUCER_WARPS
+#define FFWD_PRODUCER_WARPS 16
+#endif
 #include "gemm_sm100.cuh"
 
 namespace ffwd {
@@ -23,7 +28,8 @@ constexpr int kBBytes = UP_BN * BK * 2;  // 32 KiB per stage
 
 __global__ void __launch_bounds__(kThreads, 1)
     up_proj_kernel(const __grid_constant__ CUtensorMap tm_x,
-                   const __grid_constant__ CUtensorMap tm_w, GemmArgs a) {
+                   const __grid_constant__ CUtensorMap tm_w,
+                   const __grid_constant__ CUtensorMap tm_wt, GemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   Smem<kBBytes> sm(smem_raw);
   const int warp = threadIdx.x >> 5;
@@ -31,6 +37,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_x);
     tma_prefetch_desc(&tm_w);
+    tma_prefetch_desc(&tm_wt);
   }
   prologue(sm, warp);
   const uint32_t tmem = sm.bar->tmem_base;
@@ -48,32 +55,45 @@ __global__ void __launch_bounds__(kThreads, 1)
       const Tile tl = a.up_tiles[t];
       if (tl.b < 0) continue;
       const BlockMeta m = a.meta[tl.b];
-      for (int i = static_cast<int>(lane); i < R; i += 32) {
-        const int j = R * warp + i;  // B row within the tile
-        int r;
-        if (tl.kind == 0) {
-          const int half = j >> 7;  // 0 = gate rows, 1 = up rows
-          r = neuron_at(m, a.idx, a.ld_idx, tl.n0 + (j & 127)) + half * a.f_local;
-        } else {
-          r = 2 * a.f_local + tl.n0 + j;
+      // Contiguous B rows (dense blocks' identity index, compensator rows) take the
+      // 2-D tile path: two 128-row boxes issued by warp 0, ~1.5x the gather4 rate.
+      const bool contiguous = tl.kind != 0 || m.idx_row < 0;
+      if (!contiguous) {
+        for (int i = static_cast<int>(lane); i < R; i += 32) {
+          const int j = R * warp + i;  // B row within the tile
+          const int half = j >> 7;     // 0 = gate rows, 1 = up rows
+          rows[i] = neuron_at(m, a.idx, a.ld_idx, tl.n0 + (j & 127)) + half * a.f_local;
         }
-        rows[i] = r;
       }
       __syncwarp();
       if (lane == 0) {
-        const uint32_t bytes = R * BK * 2 + (warp == 0 ? kABytes : 0);
+        uint32_t bytes = contiguous ? 0 : R * BK * 2;
+        if (warp == 0) bytes += kABytes + (contiguous ? UP_BN * BK * 2 : 0);
+        const int r0 = tl.kind != 0 ? 2 * a.f_local + tl.n0 : tl.n0;  // first box row
+        const int r1 = tl.kind != 0 ? r0 + 128 : a.f_local + tl.n0;    // second box row
         const int4* rq = reinterpret_cast<const int4*>(rows);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&sm.bar->empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&sm.bar->full[stage], bytes);
-          if (warp == 0)
+          if (bytes)
+            mbar_arrive_expect_tx(&sm.bar->full[stage], bytes);
+          else
+            mbar_arrive(&sm.bar->full[stage]);
+          if (warp == 0) {
             tma_load_2d(&tm_x, &sm.bar->full[stage], sm.a_stage(stage), kb * BK, m.tok0, pol_x);
-          uint8_t* dst = sm.b_stage(stage) + warp * R * 128;
+            if (contiguous) {
+              tma_load_2d(&tm_wt, &sm.bar->full[stage], sm.b_stage(stage), kb * BK, r0, pol_w);
+              tma_load_2d(&tm_wt, &sm.bar->full[stage], sm.b_stage(stage) + 128 * 128, kb * BK,
+                          r1, pol_w);
+            }
+          }
+          if (!contiguous) {
+            uint8_t* dst = sm.b_stage(stage) + warp * R * 128;
 #pragma unroll
-          for (int q = 0; q < R / 4; ++q) {
-            const int4 r = rq[q];
-            tma_gather4(&tm_w, &sm.bar->full[stage], dst + q * 512, kb * BK, r.x, r.y, r.z, r.w,
-                        pol_w);
+            for (int q = 0; q < R / 4; ++q) {
+              const int4 r = rq[q];
+              tma_gather4(&tm_w, &sm.bar->full[stage], dst + q * 512, kb * BK, r.x, r.y, r.z,
+                          r.w, pol_w);
+            }
           }
           advance(stage, phase);
         }
@@ -111,18 +131,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t tb = tmem + acc * UP_BN + (static_cast<uint32_t>(ew * 32) << 16);
       __nv_bfloat16* hrow = static_cast<__nv_bfloat16*>(a.h) +
                             static_cast<size_t>(tl.b * kBlockTokens + row) * a.hcols;
+      // 16-column chunks keep the epilogue's register footprint small enough for
+      // 16 producer warps in the same CTA.
       if (tl.kind == 0) {
 #pragma unroll 1
-        for (int c = 0; c < 128; c += 32) {
+        for (int c = 0; c < 128; c += 16) {
           const int pos = tl.n0 + c;
           if (pos >= m.kpad) break;
-          uint32_t g[32], u[32];
-          tmem_ld32(tb + c, g);
-          tmem_ld32(tb + 128 + c, u);
+          uint32_t g[16], u[16];
+          tmem_ld16(tb + c, g);
+          tmem_ld16(tb + 128 + c, u);
           tmem_ld_wait();
-          uint32_t packed[16];
+          uint32_t packed[8];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
+          for (int j = 0; j < 8; ++j) {
             float h0 = silu_f32(__uint_as_float(g[2 * j])) * __uint_as_float(u[2 * j]);
             float h1 = silu_f32(__uint_as_float(g[2 * j + 1])) * __uint_as_float(u[2 * j + 1]);
             if (pos + 2 * j >= m.kcount) h0 = 0.0f;
@@ -130,29 +152,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             packed[j] = pack_bf16x2(h0, h1);
           }
           uint4* dst = reinterpret_cast<uint4*>(hrow + pos);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2],
-                                packed[4 * j + 3]);
+          dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+          dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
         }
       } else {
 #pragma unroll 1
-        for (int c = 0; c < UP_BN; c += 32) {
+        for (int c = 0; c < UP_BN; c += 16) {
           const int col = tl.n0 + c;
           if (col >= m.comp) break;
-          uint32_t g[32];
-          tmem_ld32(tb + c, g);
+          uint32_t g[16];
+          tmem_ld16(tb + c, g);
           tmem_ld_wait();
-          uint32_t packed[16];
+          uint32_t packed[8];
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
+          for (int j = 0; j < 8; ++j)
             packed[j] = pack_bf16x2(silu_f32(__uint_as_float(g[2 * j])),
                                     silu_f32(__uint_as_float(g[2 * j + 1])));
           uint4* dst = reinterpret_cast<uint4*>(hrow + m.kpad + col);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2],
-                                packed[4 * j + 3]);
+          dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+          dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
         }
       }
       tc_fence_before();
@@ -167,10 +185,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 }  // namespace
 
 cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s) {
-  CUtensorMap tx, tw;
+  CUtensorMap tx, tw, twt;
   if (encode_tmap_2d_bf16(&tx, a.x, a.d, a.T, BK, BM) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   if (encode_tmap_2d_bf16(&tw, a.wgu_t, a.d, a.wgu_rows, BK, 1) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  if (encode_tmap_2d_bf16(&twt, a.wgu_t, a.d, a.wgu_rows, BK, 128) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   constexpr size_t smem = smem_bytes<kBBytes>();
   static bool attr = false;
@@ -181,7 +201,7 @@ cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s) {
     attr = true;
   }
   const int grid = a.num_sms < a.up_cap ? a.num_sms : a.up_cap;
-  up_proj_kernel<<<grid, kThreads, smem, s>>>(tx, tw, a);
+  up_proj_kernel<<<grid, kThreads, smem, s>>>(tx, tw, twt, a);
   return cudaGetLastError();
 }
 

@@ -15,7 +15,7 @@
 
 using namespace ffwd;
 
-constexpr int kMaxStages = 6;
+constexpr int kMaxStages = 4;
 constexpr int kStageBytes = 32768;
 
 struct Bars {
@@ -26,15 +26,16 @@ struct Bars {
 // stage issued by one thread; mode 2: 64 gather4 issued by 4 warps (16 each).
 __global__ void __launch_bounds__(512, 1)
     tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_constant__ CUtensorMap tm_g,
+               const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_a2,
                const int* __restrict__ rows_all, int n_rowsets, int iters, int stages, int mode,
-               int kdim, unsigned long long* cycles, const __nv_bfloat16* wptr) {
+               int kdim, unsigned long long* cycles, const __nv_bfloat16* wptr, int share_a) {
   extern __shared__ uint8_t raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-  Bars* bars = reinterpret_cast<Bars*>(base + kMaxStages * kStageBytes);
+  Bars* bars = reinterpret_cast<Bars*>(base + kMaxStages * kStageBytes + 1024 + kMaxStages * 16384);
   __shared__ int srows[256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // barrier arrivals per fill: TMA modes count issuing warps; cp.async modes count threads
-  const int nwarps_issue = mode == 7 ? 128 : mode == 8 ? 256 : mode == 9 ? 128 + 2 :
+  const int nwarps_issue = mode == 12 ? 8 : mode == 10 ? 8 : mode == 11 ? 16 : mode == 7 ? 128 : mode == 8 ? 256 : mode == 9 ? 128 + 2 :
                            mode == 5 ? 8 : (mode == 6 ? 16 : (mode >= 2 ? 4 : 1));
   if (threadIdx.x == 0) {
     for (int i = 0; i < kMaxStages; ++i) mbar_init(&bars->full[i], nwarps_issue);
@@ -57,7 +58,7 @@ __global__ void __launch_bounds__(512, 1)
       phase_bits ^= 1u << s;
     }
     __syncthreads();
-    const int kb = (it + blockIdx.x) % nk;
+    const int kb = (it + (share_a > 1 ? blockIdx.x / share_a : blockIdx.x)) % nk;
     uint8_t* dst = base + s * kStageBytes;
     if (mode == 0) {
       if (threadIdx.x == 0) {
@@ -94,6 +95,45 @@ __global__ void __launch_bounds__(512, 1)
         for (int q = 0; q < 16; ++q)
           tma_gather4(&tm_g, &bars->full[s], dst + (warp * 16 + q) * 512, kb * 64, r[q].x,
                       r[q].y, r[q].z, r[q].w, pol);
+      }
+    } else if (mode == 12) {
+      uint32_t cs, crank;
+      asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(cs));
+      asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+      if (warp < 8 && lane == 0) {
+        mbar_arrive_expect_tx(&bars->full[s], kStageBytes / 8 + (warp == 0 ? 16384 : 0));
+        if (warp == 0) {
+          const uint32_t rows_each = 128 / cs;
+          uint8_t* adst = base + kMaxStages * kStageBytes + 1024 + s * 16384 + crank * rows_each * 128;
+          const uint16_t mask = (1u << cs) - 1;
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(adst)),
+              "l"(reinterpret_cast<uint64_t>(&tm_a2)), "r"(smem_u32(&bars->full[s])), "r"(kb * 64),
+              "r"(int(((blockIdx.x / cs) * 128 + crank * rows_each) % 16384)), "h"(mask)
+              : "memory");
+        }
+        const int4* rq = reinterpret_cast<const int4*>(srows) + warp * 8;
+        for (int q = 0; q < 8; ++q) {
+          const int4 r = rq[q];
+          tma_gather4(&tm_g, &bars->full[s], dst + (warp * 8 + q) * 512, kb * 64, r.x, r.y, r.z,
+                      r.w, pol);
+        }
+      }
+      asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else if (mode >= 10) {  // K2-like stage: 32 KiB gathered + 16 KiB A tile
+      const int nw = mode == 10 ? 8 : 16, per = 64 / nw;
+      if (warp < nw && lane == 0) {
+        mbar_arrive_expect_tx(&bars->full[s], kStageBytes / nw + (warp == 0 ? 16384 : 0));
+        if (warp == 0)
+          tma_load_2d(&tm_a, &bars->full[s], base + kMaxStages * kStageBytes + 1024 + s * 16384,
+                      kb * 64, ((share_a > 1 ? blockIdx.x / share_a : blockIdx.x) * 128) % 16384, pol);
+        const int4* rq = reinterpret_cast<const int4*>(srows) + warp * per;
+        for (int q = 0; q < per; ++q) {
+          const int4 r = rq[q];
+          tma_gather4(&tm_g, &bars->full[s], dst + (warp * per + q) * 512, kb * 64, r.x, r.y,
+                      r.z, r.w, pol);
+        }
       }
     } else if (mode >= 7) {  // cp.async 16 B per thread (LDGSTS), swizzled like TMA
       const int nthr = mode == 7 ? 128 : (mode == 8 ? 256 : 128);
@@ -173,7 +213,18 @@ int main(int argc, char** argv) {
   cuuint32_t box_t[2] = {64, 256}, box_g[2] = {64, 1}, es[2] = {1, 1};
   enc(&tile, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box_t, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  const int promo = argc > 2 ? atoi(argv[2]) : 3;  // 0 none, 1 64B, 2 128B, 3 256B
+  CUtensorMap amap;
+  cuuint32_t box_a[2] = {64, 128};
+  enc(&amap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box_a, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const int promo = argc > 2 ? atoi(argv[2]) : 3;
+  const int share = argc > 3 ? atoi(argv[3]) : 1;  // CTAs sharing one A tile stream
+  const int csz = argc > 4 ? atoi(argv[4]) : 2;     // cluster size for mode 12
+  CUtensorMap amap2;
+  cuuint32_t box_a2[2] = {64, cuuint32_t(128 / csz)};
+  enc(&amap2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box_a2, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  printf("A shared by %d CTAs\n", share);  // 0 none, 1 64B, 2 128B, 3 256B
   enc(&g, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box_g, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
       CU_TENSOR_MAP_SWIZZLE_128B, (CUtensorMapL2promotion)promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   printf("gather promotion %d\n", promo);
@@ -193,22 +244,32 @@ int main(int argc, char** argv) {
   cudaMemcpy(drows, hrows.data(), hrows.size() * 4, cudaMemcpyHostToDevice);
   unsigned long long* dcyc;
   cudaMalloc(&dcyc, 148 * 8);
-  const size_t smem = 1024 + kMaxStages * kStageBytes + sizeof(Bars);
+  const size_t smem = 1024 + kMaxStages * kStageBytes + 1024 + kMaxStages * 16384 + sizeof(Bars);
   cudaFuncSetAttribute(tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
-  const char* names[10] = {"tile 64x256", "gather4 x64 (1 thread)", "gather4 x64 (4 warps)",
+  const char* names[13] = {"tile 64x256", "gather4 x64 (1 thread)", "gather4 x64 (4 warps)",
                           "gather4 4w preload", "gather4 4w x16 lanes", "gather4 8 warps",
                           "gather4 16 warps", "cp.async 128 thr", "cp.async 256 thr",
-                          "half gather4 + half cp.async"};
-  for (int mode = 0; mode < 10; ++mode) {
+                          "half gather4 + half cp.async", "K2 stage, 8 warps", "K2 stage, 16 warps", "K2 stage 8w A-multicast"};
+  for (int mode = 0; mode < 13; ++mode) {
     if (mode == 1 || mode == 3 || mode == 4 || mode == 7 || mode == 9) continue;
     for (int stages : {4}) {
-      tma_kernel<<<148, 512, smem>>>(tile, g, drows, n_sets, 50, stages, mode, kdim, dcyc, (const __nv_bfloat16*)w);
+      if (mode != 12) tma_kernel<<<148, 512, smem>>>(tile, g, amap, amap2, drows, n_sets, 50, stages, mode, kdim, dcyc, (const __nv_bfloat16*)w, share);
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
       cudaEventRecord(e0);
-      tma_kernel<<<148, 512, smem>>>(tile, g, drows, n_sets, iters, stages, mode, kdim, dcyc, (const __nv_bfloat16*)w);
+      if (mode == 12) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(148); cfg.blockDim = dim3(512); cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = csz; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        cfg.attrs = at; cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, tma_kernel, tile, g, amap, amap2, (const int*)drows, n_sets, iters,
+                           stages, mode, kdim, dcyc, (const __nv_bfloat16*)w, share);
+      } else
+      tma_kernel<<<148, 512, smem>>>(tile, g, amap, amap2, drows, n_sets, iters, stages, mode, kdim, dcyc, (const __nv_bfloat16*)w, share);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
@@ -218,7 +279,7 @@ int main(int argc, char** argv) {
       double avg = 0;
       for (auto v : c) avg += v;
       avg /= 148;
-      const double bytes = 148.0 * iters * kStageBytes;
+      const double bytes = 148.0 * iters * (kStageBytes + (mode >= 10 ? 16384 : 0));
       printf("%-24s stages=%d span=%d: %.1f cyc/stage/SM, %.2f TB/s aggregate (%.3f ms) %s\n",
              names[mode], stages, span, avg / iters, bytes / (ms * 1e-3) / 1e12, ms,
              cudaGetErrorString(cudaGetLastError()));
