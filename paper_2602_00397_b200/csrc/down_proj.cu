@@ -16,6 +16,18 @@
 #endif
 #include "gemm_sm100.cuh"
 
+// L2 policies (A/B tuning knobs): 0 evict_normal, 1 evict_first, 2 evict_last.
+#ifndef FFWD_K3_H_POLICY
+#define FFWD_K3_H_POLICY 2
+#endif
+#ifndef FFWD_K3_W_POLICY
+#define FFWD_K3_W_POLICY 0
+#endif
+// 1: residual loads / Y and next-X stores bypass L2 residency (.cs streaming)
+#ifndef FFWD_K3_STREAM_EPI
+#define FFWD_K3_STREAM_EPI 0
+#endif
+
 namespace ffwd {
 
 namespace {
@@ -46,8 +58,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < kProducerWarps) {
     // ---------------- producers: warp w gathers K rows [Q w, Q w + Q) of every stage
     constexpr int Q = BK / kProducerWarps;  // K rows per producer warp (multiple of 4)
-    const uint64_t pol_h = policy_evict_last();
-    const uint64_t pol_w = policy_evict_normal();
+    auto pol = [](int k) {
+      return k == 1 ? policy_evict_first() : (k == 2 ? policy_evict_last() : policy_evict_normal());
+    };
+    const uint64_t pol_h = pol(FFWD_K3_H_POLICY);
+    const uint64_t pol_w = pol(FFWD_K3_W_POLICY);
     int* rows = sm.bar->rows[warp];
     uint32_t stage = 0, phase = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -59,10 +74,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int p = kb * BK + Q * warp + static_cast<int>(lane % Q);
         return p < m.kpad ? neuron_at(m, a.idx, a.ld_idx, p) : a.f_local + (p - m.kpad);
       };
-      int next = row_of(0);
+      // Neuron ids are prefetched 4 stages ahead (a register ring): an index load that
+      // misses L2 outlasts one stage, and the gathers of a stage cannot issue without it.
+      int r0 = row_of(0), r1 = nk > 1 ? row_of(1) : 0, r2 = nk > 2 ? row_of(2) : 0,
+          r3 = nk > 3 ? row_of(3) : 0;
       for (int kb = 0; kb < nk; ++kb) {
-        const int cur = next;
-        if (kb + 1 < nk) next = row_of(kb + 1);  // prefetch: consumed next iteration
+        const int cur = r0;
+        r0 = r1;
+        r1 = r2;
+        r2 = r3;
+        if (kb + 4 < nk) r3 = row_of(kb + 4);
         // Contiguous K rows (identity index of dense blocks, compensator rows past kpad)
         // take the 2-D tile path: one 64-row box per column atom, issued by warp 0.
         const bool contiguous = m.idx_row < 0 || kb * BK >= m.kpad;
@@ -149,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float4* res = reinterpret_cast<const float4*>(a.residual + row_off + c);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const float4 r = res[j];
+              const float4 r = FFWD_K3_STREAM_EPI ? __ldcs(res + j) : res[j];
               o[4 * j] += r.x;
               o[4 * j + 1] += r.y;
               o[4 * j + 2] += r.z;
@@ -158,17 +179,21 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           float4* dst = reinterpret_cast<float4*>(a.y + row_off + c);
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+          for (int j = 0; j < 4; ++j) {
+            const float4 v4 = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+            if (FFWD_K3_STREAM_EPI) __stcs(dst + j, v4); else dst[j] = v4;
+          }
           if (a.x_next) {  // next layer's bf16 input
             uint4* xn = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.x_next) +
                                                  row_off + c);
 #pragma unroll
-            for (int j = 0; j < 2; ++j)
-              xn[j] = make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]),
-                                 pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
-                                 pack_bf16x2(o[8 * j + 4], o[8 * j + 5]),
-                                 pack_bf16x2(o[8 * j + 6], o[8 * j + 7]));
+            for (int j = 0; j < 2; ++j) {
+              const uint4 v4 = make_uint4(pack_bf16x2(o[8 * j], o[8 * j + 1]),
+                                          pack_bf16x2(o[8 * j + 2], o[8 * j + 3]),
+                                          pack_bf16x2(o[8 * j + 4], o[8 * j + 5]),
+                                          pack_bf16x2(o[8 * j + 6], o[8 * j + 7]));
+              if (FFWD_K3_STREAM_EPI) __stcs(xn + j, v4); else xn[j] = v4;
+            }
           }
         }
       }
