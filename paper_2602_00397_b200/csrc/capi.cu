@@ -108,6 +108,7 @@ struct Carve {
 };
 
 struct Pred {
+  float* logits;
   float* pooled;
   float* hidden;
   double* partial;
@@ -116,6 +117,7 @@ struct Pred {
 
 Pred carve_pred(Carve& c, int nb, int d, int r, int f, bool with_scores) {
   Pred p;
+  p.logits = c.take<float>(static_cast<size_t>(nb) * kBlockTokens);
   p.pooled = c.take<float>(static_cast<size_t>(nb) * d);
   p.hidden = c.take<float>(static_cast<size_t>(nb) * r);
   const size_t part = std::max(gemm_f64acc_partial_bytes(nb, d, r),
@@ -131,7 +133,7 @@ int run_predictor(const void* x, bool x_is_f32, int T, int d, int b0, int nb, co
   const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));  // predictor.py:76
   {
     StageTimer tm(kPool, s);
-    FFWD_CUDA(launch_pool(x, x_is_f32, T, d, b0, nb, query, sqrt_d, p.pooled, s),
+    FFWD_CUDA(launch_pool(x, x_is_f32, T, d, b0, nb, query, sqrt_d, p.logits, p.pooled, s),
               "pool");
   }
   {

@@ -39,11 +39,12 @@ struct PlanCounts {
 };
 
 // ------------------------------------------------------------------ K1
-// X_b read once per block (cluster-fused logits + softmax + pooled), then the two
-// f64-accumulated predictor GEMMs (DMMA, cluster split-K reduced in fixed order).
+// Attention pooling in two streaming passes over X (per-token logits, then per-block
+// softmax + pooled sum), then the two f64-accumulated predictor GEMMs (DMMA, split-K
+// partials reduced in fixed order).  `logits`: blk_count * 128 floats of scratch.
 cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begin,
-                        int blk_count, const float* query, float sqrt_d, float* pooled,
-                        cudaStream_t s);
+                        int blk_count, const float* query, float sqrt_d, float* logits,
+                        float* pooled, cudaStream_t s);
 // `partial` (nullable, gemm_f64acc_partial_bytes) enables split-K.
 size_t gemm_f64acc_partial_bytes(int M, int K, int N);
 cudaError_t launch_gemm_f64acc(const float* A, const float* B, float* C, int M, int K, int N,

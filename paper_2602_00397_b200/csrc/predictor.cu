@@ -1,25 +1,20 @@
 // K1a/K1b: the FastForward expert predictor (predictor.py:68-81), fp64-exact.
 //
-//   pool_kernel     one thread-block cluster per 128-token block; CTA r of the
-//                   cluster owns a d/cs column slice of X_b, staged once in shared
-//                   memory (X is read from HBM exactly once):
-//                     z_t = f32(q . x_t) with f64 accumulation (kernels.py:41-54):
-//                         per-slice f64 partials summed across the cluster
-//                         through DSMEM in fixed rank order;
-//                     logit_t = z_t / f32(sqrt d), a true IEEE f32 division
-//                         (predictor.py:76: matmul(...) / np.float32(np.sqrt(d)));
-//                     p = f32(softmax_f64(logits)) (kernels.py:57-80);
-//                     pooled = f32(sum_t p_t x_t), f64 accumulation (predictor.py:78).
+//   logits_kernel   one warp per token: logit_t = f32(q . x_t) / f32(sqrt d), the dot
+//                   product accumulated in f64 and rounded once (kernels.py:41-54), the
+//                   divide a true IEEE f32 division (predictor.py:76).
+//   pooled_kernel   per (block, 256 columns): p = f32(softmax_f64(logits_b))
+//                   (kernels.py:57-80), pooled = f32(sum_t p_t x_t) in f64 (:78).
+//                   Runs the blocks in reverse so the rows pass 1 read last hit L2.
 //   gemm_f64_kernel relu(f32(pooled . W1)) and f32(h . W2) (predictor.py:79-80) on
-//                   the FP64 tensor pipe (DMMA m8n8k4); K split across a cluster
-//                   and reduced through DSMEM in fixed rank order when the output
-//                   grid alone cannot fill the GPU.
+//                   the FP64 tensor pipe (DMMA m8n8k4); K split into f64 partials
+//                   reduced in fixed order when the output grid cannot fill the GPU.
 //
 // Every product is accumulated in fp64 and rounded once to f32 exactly where the
 // reference rounds, so the scores are bit-identical to it and the selected
-// indices exact.  The pool is HBM bound (X once); the GEMMs are FP64 bound
-// (tools/fp64_bench.cu: DMMA 36.9, DFMA 33 TFLOP/s on B200).
-#include <cooperative_groups.h>
+// indices exact.  The two pooling passes are HBM bound (X streamed twice, the second
+// partly from L2); the GEMMs are FP64 bound (tools/fp64_bench.cu: DMMA 36.9, DFMA
+// 33 TFLOP/s on B200).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -29,8 +24,6 @@
 
 #include "ffwd_internal.h"
 #include "sm100.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace ffwd {
 
@@ -55,150 +48,103 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
                : "memory");
 }
 
-// 1-D TMA bulk copy global -> this CTA's shared memory, completing on `bar`.
-__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(smem)),
-      "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void cluster_arrive_release() {
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ void cluster_wait_acquire() {
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
-// 8 consecutive activations as f32 (bf16 -> f32 is exact).
+// 8 consecutive activations (bf16 or f32) as packed 16 B vectors.
 template <bool kF32>
-__device__ __forceinline__ void load8(const void* p, float (&v)[8]) {
-  if constexpr (kF32) {
-    const float4 a = reinterpret_cast<const float4*>(p)[0];
-    const float4 b = reinterpret_cast<const float4*>(p)[1];
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-  } else {
-    const uint4 raw = *reinterpret_cast<const uint4*>(p);
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+struct Raw8 {
+  uint4 v[kF32 ? 2 : 1];
+  __device__ __forceinline__ void load(const void* base, size_t elem) {
+    const uint4* p = reinterpret_cast<const uint4*>(static_cast<const char*>(base) +
+                                                    elem * (kF32 ? 4 : 2));
+    v[0] = __ldg(p);
+    if constexpr (kF32) v[1] = __ldg(p + 1);
+  }
+  __device__ __forceinline__ void zero() {
+    v[0] = make_uint4(0, 0, 0, 0);
+    if constexpr (kF32) v[1] = make_uint4(0, 0, 0, 0);
+  }
+  __device__ __forceinline__ double get(int i) const {  // exact widening of element i
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(v);
+    if constexpr (kF32) return static_cast<double>(__uint_as_float(w[i]));
+    else
+      return static_cast<double>(
+          __uint_as_float((i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16)));
+  }
+};
+
+constexpr int kLogitThreads = 256;
+constexpr int kLogitWarps = kLogitThreads / 32;
+constexpr int kPoolThreads = 256;
+constexpr int kPoolCols = 512;   // per CTA: two 256-column warp halves
+constexpr int kPoolQuarters = 4; // token quarters of a block
+
+// Pass 1: logit_t = f32(q . x_t) / f32(sqrt d) for every token of the predicted blocks
+// (predictor.py:76; the matmul accumulates in f64 and rounds once, kernels.py:41-54).
+// One warp per token row, 4 x 16 B loads per lane in flight, 40 registers so 64 warps
+// per SM stay resident.  (A/B on B200, ncu, 8B/16K: this 39 us; q held in f64
+// registers with one widening per x element 49 us; q in f64 shared memory 78 us.)
+template <bool kF32>
+__global__ void __launch_bounds__(kLogitThreads)
+    logits_kernel(const void* __restrict__ x, int d, int tok0, int ntok,
+                  const float* __restrict__ query, float sqrt_d, float* __restrict__ logits) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * kLogitWarps + warp;
+  if (t >= ntok) return;
+  const size_t row = static_cast<size_t>(tok0 + t) * d;
+  const int ng = d / 8;
+  double a0 = 0.0, a1 = 0.0;
+  int g = lane;
+  for (; g + 96 < ng; g += 128) {  // 4 groups of 8 columns per lane per iteration
+    Raw8<kF32> xr[4];
+    Raw8<true> qr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) xr[u].load(x, row + 8 * static_cast<size_t>(g + 32 * u));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) qr[u].load(query, 8 * static_cast<size_t>(g + 32 * u));
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a0 = fma(qr[u].get(i), xr[u].get(i), a0);
+        a1 = fma(qr[u].get(4 + i), xr[u].get(4 + i), a1);
+      }
+  }
+  for (; g < ng; g += 32) {
+    Raw8<kF32> xr;
+    Raw8<true> qr;
+    xr.load(x, row + 8 * static_cast<size_t>(g));
+    qr.load(query, 8 * static_cast<size_t>(g));
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const float2 f = __bfloat1622float2(h[i]);
-      v[2 * i] = f.x;
-      v[2 * i + 1] = f.y;
+      a0 = fma(qr.get(i), xr.get(i), a0);
+      a1 = fma(qr.get(4 + i), xr.get(4 + i), a1);
     }
   }
+  const double z = warp_sum_f64(a0 + a1);
+  if (lane == 0) logits[t] = __fdiv_rn(static_cast<float>(z), sqrt_d);  // predictor.py:76
 }
 
-constexpr int kPoolThreads = 256;
-constexpr size_t kPoolMaxSmem = 72 * 1024;  // 3 CTAs per SM
-
-__host__ __device__ __forceinline__ int pool_slice(int d, int cs) {
-  const int w = (d + cs - 1) / cs;
-  return (w + 7) / 8 * 8;
-}
-
-// grid (cs, blk_count), cluster (cs, 1, 1).  Dynamic shared memory: the CTA's
-// query slice widened to f64, then (kCache) its [n x w] slice of X_b with a 16 B
-// padded row pitch so per-token row reads are bank-conflict free; otherwise both
-// passes read global memory (the second pass hits L2).  The pooled partials of the
-// token groups reuse the X area once it is consumed.
-template <bool kF32, bool kCache>
-__global__ void __launch_bounds__(kPoolThreads, 3)
-    pool_kernel(const void* __restrict__ x, int T, int d, int blk_begin,
-                const float* __restrict__ query, float sqrt_d, float* __restrict__ pooled) {
-  using E = std::conditional_t<kF32, float, __nv_bfloat16>;
-  constexpr int kPad = 16 / static_cast<int>(sizeof(E));
-  extern __shared__ __align__(16) uint8_t dyn[];
-  __shared__ double part2[2][kBlockTokens];
-  __shared__ double part[kBlockTokens];
-  __shared__ double probd[kBlockTokens];  // f32-rounded softmax, widened once
+// Pass 2: p = f32(softmax_f64(logits_b)) (kernels.py:57-80), recomputed by every CTA of
+// the block (128 values), then pooled_b[c] = f32(sum_t p_t x_t[c]) with f64 accumulation
+// (predictor.py:78).  grid (ceil(d / 512), blk_count); blocks run in reverse order so
+// the rows pass 1 read last are still in L2.  Warp w covers 256 columns (8 per lane,
+// half h = w & 1 of the CTA's 512) for the 32 tokens of quarter w >> 1, with 16 loads
+// of 16 B in flight per lane; the four quarter partials are added in order.
+template <bool kF32>
+__global__ void __launch_bounds__(kPoolThreads, 2)
+    pooled_kernel(const void* __restrict__ x, int T, int d, int blk_begin, int blk_count,
+                  const float* __restrict__ logits, float* __restrict__ pooled) {
+  __shared__ double probd[kBlockTokens];
   __shared__ double wred[2][4];
-  __shared__ uint64_t xbar[4];
-
-  cg::cluster_group cluster = cg::this_cluster();
-  const int cs = static_cast<int>(cluster.num_blocks());
-  const int rank = static_cast<int>(cluster.block_rank());
-  const int b = blk_begin + blockIdx.y;
-  const int tok0 = b * kBlockTokens;
+  __shared__ double red[kPoolQuarters][kPoolCols];
+  const int rel = blk_count - 1 - static_cast<int>(blockIdx.y);
+  const int tok0 = (blk_begin + rel) * kBlockTokens;
   const int n = min(kBlockTokens, T - tok0);
-  const int w = pool_slice(d, cs);
-  const int wp = w + kPad;
-  const int c0 = rank * w;
-  const int nc = max(0, min(d, c0 + w) - c0);
-  const E* xg = static_cast<const E*>(x) + static_cast<size_t>(tok0) * d + c0;
-  double* qs = reinterpret_cast<double*>(dyn);
-  uint8_t* xs_raw = dyn + static_cast<size_t>(w) * sizeof(double);
-  const E* xs = reinterpret_cast<const E*>(xs_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // Stage X_b[:, slice] with one TMA bulk copy per row, in 4 groups of 32 rows with
-  // their own mbarriers so phase 1 starts on the first rows while the rest land.
-  if constexpr (kCache) {
-    if (threadIdx.x < 4) mbar_init(&xbar[threadIdx.x], 1);
-    fence_barrier_init();
-    __syncthreads();
-    if (warp == 0 && nc > 0) {
-      const uint32_t row_bytes = static_cast<uint32_t>(nc * sizeof(E));
-      for (int grp = 0; grp < 4; ++grp) {
-        const int rows = max(0, min(32, n - 32 * grp));
-        if (lane == 0) mbar_arrive_expect_tx(&xbar[grp], row_bytes * static_cast<uint32_t>(rows));
-        __syncwarp();
-        const int t = 32 * grp + lane;
-        if (lane < rows)
-          bulk_g2s(xs_raw + static_cast<size_t>(t) * wp * sizeof(E),
-                   xg + static_cast<size_t>(t) * d, row_bytes, &xbar[grp]);
-      }
-    }
-  }
-  for (int c = threadIdx.x; c < nc; c += kPoolThreads)
-    qs[c] = static_cast<double>(__ldg(query + c0 + c));
-  __syncthreads();
-  auto row = [&](int t) -> const E* {
-    if constexpr (kCache) return xs + static_cast<size_t>(t) * wp;
-    else return xg + static_cast<size_t>(t) * d;
-  };
-
-  // ---- slice partial of z_t = q . x_t (f64): thread = (token, half of the slice);
-  // the query is a shared-memory broadcast, two chains per thread.
-  {
-    const int t = threadIdx.x % kBlockTokens, h = threadIdx.x / kBlockTokens;
-    const int ng = nc / 8, g_lo = h * (ng / 2), g_hi = h ? ng : ng / 2;
-    double a0 = 0.0, a1 = 0.0;
-    if constexpr (kCache) {
-      if (nc > 0) mbar_wait(&xbar[t >> 5], 0);  // this row's group has landed
-    }
-    if (t < n) {
-      const E* xr = row(t);
-      for (int g = g_lo; g < g_hi; ++g) {
-        float xv[8];
-        load8<kF32>(xr + 8 * g, xv);
-        const double* q = qs + 8 * g;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          a0 = fma(q[i], static_cast<double>(xv[i]), a0);
-          a1 = fma(q[4 + i], static_cast<double>(xv[4 + i]), a1);
-        }
-      }
-    }
-    part2[h][t] = a0 + a1;
-  }
-  __syncthreads();
-  if (threadIdx.x < kBlockTokens) part[threadIdx.x] = part2[0][threadIdx.x] + part2[1][threadIdx.x];
-  cluster.sync();
-
-  // ---- logits (same in every CTA: fixed rank order), softmax over 4 warps
-  double l = -INFINITY;
-  if (threadIdx.x < n) {
-    double z = 0.0;
-    for (int r = 0; r < cs; ++r) z += *cluster.map_shared_rank(&part[threadIdx.x], r);
-    l = static_cast<double>(__fdiv_rn(static_cast<float>(z), sqrt_d));  // predictor.py:76
-  }
-  cluster_arrive_release();  // done reading the peers' partials
-  const double wm = warp_max_f64(l);  // kernels.py:57-80 in f64, rounded to f32
+  // ---- softmax over the block's logits (f64, max-subtracted), rounded to f32
+  const double l = threadIdx.x < n ? static_cast<double>(logits[rel * kBlockTokens + threadIdx.x])
+                                   : -INFINITY;
+  const double wm = warp_max_f64(l);
   if (warp < 4 && lane == 0) wred[0][warp] = wm;
   __syncthreads();
   const double m = fmax(fmax(wred[0][0], wred[0][1]), fmax(wred[0][2], wred[0][3]));
@@ -206,48 +152,51 @@ __global__ void __launch_bounds__(kPoolThreads, 3)
   const double ws = warp_sum_f64(e);
   if (warp < 4 && lane == 0) wred[1][warp] = ws;
   __syncthreads();
-  if (threadIdx.x < n) {
+  if (threadIdx.x < kBlockTokens) {
     const double sum = ((wred[1][0] + wred[1][1]) + wred[1][2]) + wred[1][3];
-    probd[threadIdx.x] = static_cast<double>(static_cast<float>(e / sum));
+    probd[threadIdx.x] =
+        threadIdx.x < n ? static_cast<double>(static_cast<float>(e / sum)) : 0.0;
   }
   __syncthreads();
 
-  // ---- pooled slice: 8 columns per thread x token groups, f64 partials summed in
-  // group order (predictor.py:78).
-  const int ng = nc / 8;                                       // 8-column groups
-  const int cgp = min(kPoolThreads, max(32, (ng + 31) / 32 * 32));  // threads per token group
-  const int tgs = kPoolThreads / cgp;                          // token groups
-  const int per = (n + tgs - 1) / tgs;
-  const int tg = threadIdx.x / cgp;
-  double* red = reinterpret_cast<double*>(xs_raw);             // [tgs][cgp * 8] (aliases X)
-  for (int g0 = 0; g0 < ng; g0 += cgp) {
-    const int g = g0 + threadIdx.x % cgp;
-    double acc[8];
+  // ---- pooled partials
+  const int half = warp & 1, quarter = warp >> 1;
+  const int cl = half * 256 + lane * 8;  // column within the CTA's 512
+  const int c = blockIdx.x * kPoolCols + cl;
+  double acc[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] = 0.0;
-    if (tg < tgs && g < ng) {
-      const int t_hi = min(n, tg * per + per);
-      for (int t = tg * per; t < t_hi; ++t) {
-        float xv[8];
-        load8<kF32>(row(t) + 8 * g, xv);
-        const double pt = probd[t];
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+  if (c < d) {
+    constexpr int kPer = kBlockTokens / kPoolQuarters;  // 32 tokens per warp
+    constexpr int kBatch = kF32 ? 8 : 16;               // tokens in flight per lane
+#pragma unroll 1
+    for (int t0 = quarter * kPer; t0 < quarter * kPer + kPer; t0 += kBatch) {
+      Raw8<kF32> xr[kBatch];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = fma(pt, static_cast<double>(xv[i]), acc[i]);
+      for (int u = 0; u < kBatch; ++u) {
+        if (t0 + u < n) xr[u].load(x, static_cast<size_t>(tok0 + t0 + u) * d + c);
+        else xr[u].zero();
+      }
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const double pt = probd[t0 + u];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = fma(pt, xr[u].get(i), acc[i]);
       }
     }
-    __syncthreads();  // X (possibly aliased by `red`) fully consumed
-    if (tg < tgs)
-#pragma unroll
-      for (int i = 0; i < 8; ++i) red[tg * cgp * 8 + (threadIdx.x % cgp) * 8 + i] = acc[i];
-    __syncthreads();
-    for (int c = threadIdx.x; c < min(cgp, ng - g0) * 8; c += kPoolThreads) {
-      double v = 0.0;
-      for (int q = 0; q < tgs; ++q) v += red[q * cgp * 8 + c];
-      pooled[static_cast<size_t>(blockIdx.y) * d + c0 + g0 * 8 + c] = static_cast<float>(v);
-    }
-    __syncthreads();
   }
-  cluster_wait_acquire();  // peers may still be reading `part`
+#pragma unroll
+  for (int i = 0; i < 8; ++i) red[quarter][cl + i] = acc[i];
+  __syncthreads();
+  for (int j = threadIdx.x; j < kPoolCols; j += kPoolThreads) {
+    const int col = blockIdx.x * kPoolCols + j;
+    if (col < d) {
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < kPoolQuarters; ++q) v += red[q][j];
+      pooled[static_cast<size_t>(rel) * d + col] = static_cast<float>(v);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ f64 GEMM
@@ -390,85 +339,25 @@ int gemm_splits(int M, int K, int N) {
   return splits;
 }
 
-int g_pool_cluster = 0;  // resolved on first use: 16 when the device schedules it, else 8
-
-template <bool kF32, bool kCache>
-cudaError_t launch_pool_t(const void* x, int T, int d, int blk_begin, int blk_count,
-                          const float* query, float sqrt_d, float* pooled, int cs, size_t smem,
-                          cudaStream_t s) {
-  auto kern = pool_kernel<kF32, kCache>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(kPoolMaxSmem));
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(cs, blk_count, 1);
-  cfg.blockDim = dim3(kPoolThreads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cs;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, x, T, d, blk_begin, query, sqrt_d, pooled);
-}
-
 }  // namespace
 
 cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begin, int blk_count,
-                        const float* query, float sqrt_d, float* pooled, cudaStream_t s) {
+                        const float* query, float sqrt_d, float* logits, float* pooled,
+                        cudaStream_t s) {
   if (blk_count <= 0) return cudaSuccess;
-  if (g_pool_cluster == 0) {
-    // Prefer 16-CTA clusters (a 64 KiB bf16 slice per CTA at d = 4096, 2-3 CTAs per
-    // SM); fall back to the portable 8 if the device cannot schedule them.
-    int n16 = 0;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(16, 1, 1);
-    cfg.blockDim = dim3(kPoolThreads, 1, 1);
-    cfg.dynamicSmemBytes = 68 * 1024;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 16;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    auto kern = pool_kernel<false, true>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kPoolMaxSmem));
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (cudaOccupancyMaxActiveClusters(&n16, kern, &cfg) != cudaSuccess) n16 = 0;
-    cudaGetLastError();
-    g_pool_cluster = n16 > 0 ? 16 : 8;
+  const int tok0 = blk_begin * kBlockTokens;
+  const int ntok = std::min(T, (blk_begin + blk_count) * kBlockTokens) - tok0;
+  const dim3 g1((ntok + kLogitWarps - 1) / kLogitWarps);
+  const dim3 g2((d + kPoolCols - 1) / kPoolCols, blk_count);
+  if (x_is_f32) {
+    logits_kernel<true><<<g1, kLogitThreads, 0, s>>>(x, d, tok0, ntok, query, sqrt_d, logits);
+    pooled_kernel<true><<<g2, kPoolThreads, 0, s>>>(x, T, d, blk_begin, blk_count, logits, pooled);
+  } else {
+    logits_kernel<false><<<g1, kLogitThreads, 0, s>>>(x, d, tok0, ntok, query, sqrt_d, logits);
+    pooled_kernel<false><<<g2, kPoolThreads, 0, s>>>(x, T, d, blk_begin, blk_count, logits,
+                                                     pooled);
   }
-  const int cs = d >= 1024 ? g_pool_cluster : 8;
-  const int w = pool_slice(d, cs);
-  const size_t esz = x_is_f32 ? sizeof(float) : sizeof(__nv_bfloat16);
-  const size_t xbytes = static_cast<size_t>(kBlockTokens) * (w + 16 / esz) * esz;
-  const size_t qbytes = static_cast<size_t>(w) * sizeof(double);
-  const bool cache = qbytes + xbytes <= kPoolMaxSmem;
-  const size_t red = kPoolThreads * 8 * sizeof(double);  // pooled partials (alias X)
-  const size_t smem = qbytes + (cache ? std::max(xbytes, red) : red);
-  if (x_is_f32)
-    return cache ? launch_pool_t<true, true>(x, T, d, blk_begin, blk_count, query, sqrt_d, pooled,
-                                             cs, smem, s)
-                 : launch_pool_t<true, false>(x, T, d, blk_begin, blk_count, query, sqrt_d,
-                                              pooled, cs, smem, s);
-  return cache ? launch_pool_t<false, true>(x, T, d, blk_begin, blk_count, query, sqrt_d, pooled,
-                                            cs, smem, s)
-               : launch_pool_t<false, false>(x, T, d, blk_begin, blk_count, query, sqrt_d, pooled,
-                                             cs, smem, s);
+  return cudaGetLastError();
 }
 
 size_t gemm_f64acc_partial_bytes(int M, int K, int N) {

@@ -1,8 +1,9 @@
 // K1c: per-block top-k over the predictor scores (kernels.py:139-149 topk_indices,
 // sparse.py:49-55 build_mask).
 //
-// One CTA per block row.  Radix select over order-preserving 32-bit keys finds
-// the k-th largest key in four 8-bit passes (histograms in shared memory), then
+// One CTA per block row; the row's keys are staged once in shared memory.  Radix
+// select over order-preserving 32-bit keys finds the k-th largest key in three passes
+// (12 + 12 + 8 bit digits, histograms in shared memory), then
 // a block-wide scan compacts the kept set in index order, so the output is
 // ascending like np.sort(argsort(-s, kind="stable")[:k]).  Ties go to the lower
 // index, -0.0 == +0.0, NaN ranks below every number (NumPy sorts NaN last).
@@ -57,85 +58,107 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot, int* t
   return r;
 }
 
+// Radix digits, most significant first: 12 + 12 + 8 bits.  A 12-bit first digit
+// spreads scores of similar magnitude (same sign and exponent) over many bins, which
+// keeps the shared-memory histogram atomics nearly conflict free.
+__host__ __device__ constexpr int digit_bits(int pass) { return pass == 2 ? 8 : 12; }
+__host__ __device__ constexpr int digit_shift(int pass) { return pass == 0 ? 20 : (pass == 1 ? 8 : 0); }
+constexpr int kBins = 4096;
+constexpr int kBinsPerThread = kBins / kTopkThreads;  // 4
+
+// kCached: the row's keys are staged once in shared memory (f * 4 bytes), else every
+// pass re-reads the scores (from L2) -- only for very wide rows.
+template <bool kCached>
 __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
     const float* __restrict__ scores, int f, int k, int tp_rank, int tp_size,
     int32_t* __restrict__ idx_global, int ld_global, int32_t* __restrict__ idx_local,
     int ld_local, int32_t* __restrict__ counts) {
-  __shared__ int hist[256];
+  extern __shared__ uint32_t s_keys[];
+  __shared__ int hist[kBins];
   __shared__ int warp_tot[32];
   __shared__ int s_total;
   __shared__ uint32_t s_prefix;
   __shared__ int s_remaining;
   const float* s = scores + static_cast<size_t>(blockIdx.x) * f;
   const int tid = threadIdx.x;
+  auto key_at = [&](int i) -> uint32_t {
+    if constexpr (kCached) return s_keys[i];
+    else return rank_key(__ldg(s + i));
+  };
+  if constexpr (kCached) {
+    if ((f & 3) == 0) {
+      const float4* s4 = reinterpret_cast<const float4*>(s);
+      for (int i = tid; i < f / 4; i += kTopkThreads) {
+        const float4 v = __ldg(s4 + i);
+        s_keys[4 * i] = rank_key(v.x);
+        s_keys[4 * i + 1] = rank_key(v.y);
+        s_keys[4 * i + 2] = rank_key(v.z);
+        s_keys[4 * i + 3] = rank_key(v.w);
+      }
+    } else {
+      for (int i = tid; i < f; i += kTopkThreads) s_keys[i] = rank_key(__ldg(s + i));
+    }
+  }
 
   uint32_t prefix = 0, pmask = 0;
   int remaining = k;
 #pragma unroll 1
-  for (int shift = 24; shift >= 0; shift -= 8) {
-    if (tid < 256) hist[tid] = 0;
+  for (int pass = 0; pass < 3; ++pass) {
+    const int shift = digit_shift(pass);
+    const int nb = 1 << digit_bits(pass);
+    for (int i = tid; i < nb; i += kTopkThreads) hist[i] = 0;
     __syncthreads();
     for (int i = tid; i < f; i += kTopkThreads) {
-      const uint32_t key = rank_key(s[i]);
-      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1);
+      const uint32_t key = key_at(i);
+      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & (nb - 1)], 1);
     }
     __syncthreads();
-    if (tid < 32) {
-      // lane l owns bins [255-8l-7, 255-8l]; scan from the top bin down
-      int c[8], lsum = 0;
+    // thread t owns bins [nb-1-B t-(B-1), nb-1-B t] (descending); block scan finds the
+    // bin holding the remaining-th largest key
+    const int B = (nb + kTopkThreads - 1) / kTopkThreads;
+    int c[kBinsPerThread], lsum = 0;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        c[j] = hist[255 - 8 * tid - j];
-        lsum += c[j];
-      }
-      int incl = lsum;
+    for (int j = 0; j < kBinsPerThread; ++j) {
+      const int bin = nb - 1 - B * tid - j;
+      c[j] = (j < B && bin >= 0) ? hist[bin] : 0;
+      lsum += c[j];
+    }
+    const int above = block_exclusive_scan(lsum, warp_tot, &s_total);
+    if (above < remaining && above + lsum >= remaining) {
+      int cum = above, bin = nb - 1 - B * tid;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (tid >= o) incl += t;
-      }
-      int above = incl - lsum;  // keys in higher bins than this lane's
-      const bool mine = above < remaining && incl >= remaining;
-      if (mine) {
-        int bin = 255 - 8 * tid, cum = above;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (cum + c[j] >= remaining) {
-            bin = 255 - 8 * tid - j;
-            break;
-          }
-          cum += c[j];
+      for (int j = 0; j < kBinsPerThread; ++j) {
+        if (j < B && cum + c[j] >= remaining) {
+          bin = nb - 1 - B * tid - j;
+          break;
         }
-        s_prefix = prefix | (static_cast<uint32_t>(bin) << shift);
-        s_remaining = remaining - cum;
+        cum += c[j];
       }
+      s_prefix = prefix | (static_cast<uint32_t>(bin) << shift);
+      s_remaining = remaining - cum;
     }
     __syncthreads();
     prefix = s_prefix;
     remaining = s_remaining;
-    pmask |= 255u << shift;
+    pmask |= static_cast<uint32_t>(nb - 1) << shift;
     __syncthreads();
   }
-  const uint32_t thr = prefix;  // key of the k-th largest score
+  const uint32_t thr = prefix;    // key of the k-th largest score
   const int need_eq = remaining;  // how many keys == thr to keep (lowest index first)
 
   // -- compaction in index order: contiguous chunk per thread
   const int per = (f + kTopkThreads - 1) / kTopkThreads;
   const int lo = min(f, tid * per), hi = min(f, lo + per);
-  int gt = 0, eq = 0;
-  for (int i = lo; i < hi; ++i) {
-    const uint32_t key = rank_key(s[i]);
-    gt += key > thr;
-    eq += key == thr;
-  }
+  int eq = 0;
+  for (int i = lo; i < hi; ++i) eq += key_at(i) == thr;
   const int eq_before = block_exclusive_scan(eq, warp_tot, &s_total);
-  int take_eq = min(eq, max(0, need_eq - eq_before));
-  // first pass over the chunk: count kept (global and rank-local)
+  const int take_eq = min(eq, max(0, need_eq - eq_before));
+  // count kept (global and rank-local)
   int kept = 0, kept_loc = 0;
   {
     int te = take_eq;
     for (int i = lo; i < hi; ++i) {
-      const uint32_t key = rank_key(s[i]);
+      const uint32_t key = key_at(i);
       bool keep = key > thr;
       if (!keep && key == thr && te > 0) {
         keep = true;
@@ -152,7 +175,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
   if (tid == kTopkThreads - 1 && counts != nullptr) counts[blockIdx.x] = pos_loc + kept_loc;
   int p = pos, pl = pos_loc, te = take_eq;
   for (int i = lo; i < hi; ++i) {
-    const uint32_t key = rank_key(s[i]);
+    const uint32_t key = key_at(i);
     bool keep = key > thr;
     if (!keep && key == thr && te > 0) {
       keep = true;
@@ -168,14 +191,32 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
   }
 }
 
+constexpr size_t kTopkMaxSmem = 200 * 1024;
+
 }  // namespace
 
 cudaError_t launch_topk(const float* scores, int n_rows, int f, int k, int tp_rank, int tp_size,
                         int32_t* idx_global, int ld_global, int32_t* idx_local, int ld_local,
                         int32_t* counts, cudaStream_t s) {
   if (n_rows <= 0) return cudaSuccess;
-  topk_kernel<<<n_rows, kTopkThreads, 0, s>>>(scores, f, k, tp_rank, tp_size, idx_global,
-                                              ld_global, idx_local, ld_local, counts);
+  const size_t smem = static_cast<size_t>(f) * sizeof(uint32_t);
+  if (smem <= kTopkMaxSmem) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(topk_kernel<true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(kTopkMaxSmem));
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    topk_kernel<true><<<n_rows, kTopkThreads, smem, s>>>(scores, f, k, tp_rank, tp_size,
+                                                         idx_global, ld_global, idx_local,
+                                                         ld_local, counts);
+  } else {
+    topk_kernel<false><<<n_rows, kTopkThreads, 0, s>>>(scores, f, k, tp_rank, tp_size,
+                                                       idx_global, ld_global, idx_local,
+                                                       ld_local, counts);
+  }
   return cudaGetLastError();
 }
 

@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(512, 1)
   __shared__ int srows[256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // barrier arrivals per fill: TMA modes count issuing warps; cp.async modes count threads
-  const int nwarps_issue = mode == 12 ? 8 : mode == 10 ? 8 : mode == 11 ? 16 : mode == 7 ? 128 : mode == 8 ? 256 : mode == 9 ? 128 + 2 :
+  const int nwarps_issue = (mode == 13 || mode == 14) ? 16 : mode == 12 ? 8 : mode == 10 ? 8 : mode == 11 ? 16 : mode == 7 ? 128 : mode == 8 ? 256 : mode == 9 ? 128 + 2 :
                            mode == 5 ? 8 : (mode == 6 ? 16 : (mode >= 2 ? 4 : 1));
   if (threadIdx.x == 0) {
     for (int i = 0; i < kMaxStages; ++i) mbar_init(&bars->full[i], nwarps_issue);
@@ -121,6 +121,22 @@ __global__ void __launch_bounds__(512, 1)
         }
       }
       asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else if (mode == 13 || mode == 14) {
+      // 16 warps, same 32 KiB per stage, but each 4-row group fetches `nch` ADJACENT
+      // 128 B column chunks back to back (mode 13: 128 rows x 2 chunks, the interleaved
+      // gate/up layout; mode 14: 64 rows x 4 chunks, the down-projection pattern).
+      const int nch = mode == 13 ? 2 : 4, groups = 64 / nch, per = groups / 16;
+      const int kb2 = (it + blockIdx.x) % (kdim / (64 * nch));
+      if (warp < 16 && lane == 0) {
+        mbar_arrive_expect_tx(&bars->full[s], kStageBytes / 16);
+        const int4* rq = reinterpret_cast<const int4*>(srows) + warp * per;
+        for (int q = 0; q < per; ++q) {
+          const int4 r = rq[q];
+          for (int c = 0; c < nch; ++c)
+            tma_gather4(&tm_g, &bars->full[s], dst + ((warp * per + q) * nch + c) * 512,
+                        (kb2 * nch + c) * 64, r.x, r.y, r.z, r.w, pol);
+        }
+      }
     } else if (mode >= 10) {  // K2-like stage: 32 KiB gathered + 16 KiB A tile
       const int nw = mode == 10 ? 8 : 16, per = 64 / nw;
       if (warp < nw && lane == 0) {
@@ -247,11 +263,11 @@ int main(int argc, char** argv) {
   const size_t smem = 1024 + kMaxStages * kStageBytes + 1024 + kMaxStages * 16384 + sizeof(Bars);
   cudaFuncSetAttribute(tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
-  const char* names[13] = {"tile 64x256", "gather4 x64 (1 thread)", "gather4 x64 (4 warps)",
+  const char* names[15] = {"tile 64x256", "gather4 x64 (1 thread)", "gather4 x64 (4 warps)",
                           "gather4 4w preload", "gather4 4w x16 lanes", "gather4 8 warps",
                           "gather4 16 warps", "cp.async 128 thr", "cp.async 256 thr",
-                          "half gather4 + half cp.async", "K2 stage, 8 warps", "K2 stage, 16 warps", "K2 stage 8w A-multicast"};
-  for (int mode = 0; mode < 13; ++mode) {
+                          "half gather4 + half cp.async", "K2 stage, 8 warps", "K2 stage, 16 warps", "K2 stage 8w A-multicast", "gather4 16w 2 adjacent chunks", "gather4 16w 4 adjacent chunks"};
+  for (int mode = 0; mode < 15; ++mode) {
     if (mode == 1 || mode == 3 || mode == 4 || mode == 7 || mode == 9) continue;
     for (int stages : {4}) {
       if (mode != 12) tma_kernel<<<148, 512, smem>>>(tile, g, amap, amap2, drows, n_sets, 50, stages, mode, kdim, dcyc, (const __nv_bfloat16*)w, share);
@@ -279,7 +295,7 @@ int main(int argc, char** argv) {
       double avg = 0;
       for (auto v : c) avg += v;
       avg /= 148;
-      const double bytes = 148.0 * iters * (kStageBytes + (mode >= 10 ? 16384 : 0));
+      const double bytes = 148.0 * iters * (kStageBytes + (mode >= 10 && mode <= 12 ? 16384 : 0));
       printf("%-24s stages=%d span=%d: %.1f cyc/stage/SM, %.2f TB/s aggregate (%.3f ms) %s\n",
              names[mode], stages, span, avg / iters, bytes / (ms * 1e-3) / 1e12, ms,
              cudaGetErrorString(cudaGetLastError()));
