@@ -130,6 +130,47 @@ FFWD_API int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t,
                    size_t workspace_bytes, void* stream);
 
 /*
+ * ffwd_ffn_layer with two optional predictor inputs (NULL = as ffwd_ffn_layer):
+ *   x_pred_f32  f32 [T x d]: the predictor pools over these values instead of
+ *               x_bf16 -- the reference predictor sees the f32 RMSNorm output
+ *               (engine.py:267, 285), so exact full-model parity uses it;
+ *   logits_in   f32 [T]: per-token predictor logits f32(q . x_t) / f32(sqrt d)
+ *               (predictor.py:76) already produced by the FFN-input producer
+ *               (ffwd_rmsnorm with a query), which skips the pooling's first pass.
+ */
+FFWD_API int ffwd_ffn_layer2(const void* x_bf16, int T, int d, const void* wgu_t, const void* wd,
+                    int f_local, int rc_local, const float* query, const float* w1,
+                    const float* w2, int r, int f_global, int k, int dense_first_last,
+                    int has_comp, int tp_rank, int tp_size, float* y, const float* residual,
+                    void* x_next_bf16, int32_t* idx_global, int ld_idx_global,
+                    const float* x_pred_f32, const float* logits_in, void* workspace,
+                    size_t workspace_bytes, void* stream);
+
+/*
+ * kernels.rmsnorm (kernels.py:96-106) of the f32 residual stream x [T x d]:
+ * out = f32(x / sqrt(mean_f64(x^2) + eps) * gain), evaluated in f64 like the
+ * reference, written to out_bf16 (bf16 [T x d]) and/or out_f32.  With a
+ * predictor `query` (f32 [d]) it also writes logits[t - logit_row0] =
+ * f32(q . bf16(out_t)) / f32(sqrt d) for rows t in [logit_row0, logit_row1):
+ * the FFN-input producer fused with the predictor's first pass (engine.py:267
+ * followed by predictor.py:76).  d % 4 == 0, d <= 16384.
+ */
+FFWD_API int ffwd_rmsnorm(const float* x, const float* gain, int T, int d, double eps,
+                          void* out_bf16, float* out_f32, const float* query, float* logits,
+                          int logit_row0, int logit_row1, void* stream);
+
+/*
+ * apply_rope (engine.py:50-68) in place on Q and K of one [T x row_stride]
+ * buffer (bf16, or f32 when is_f32): Q heads at columns [0, n_heads*d_head),
+ * K heads at [k_col, k_col + n_heads*d_head).  Token t sits at position
+ * pos0 + t; cos_t / sin_t are f64 [max_pos x d_head/2] tables of
+ * cos/sin(pos * 10000^(-2i/d_head)).
+ */
+FFWD_API int ffwd_rope(void* qk, int is_f32, int T, int row_stride, int k_col, int n_heads,
+                       int d_head, const double* cos_t, const double* sin_t, int pos0,
+                       void* stream);
+
+/*
  * Per-launch device timing (CUDA events on the launching stream) for the
  * measurement harness.  Stages: 0 pool, 1 predictor W1, 2 predictor W2,
  * 3 top-k, 4 plan, 5 up-projection (K2), 6 down-projection (K3).

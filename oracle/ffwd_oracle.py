@@ -133,6 +133,23 @@ def random_layer(rng: np.random.Generator, d: int, f: int, scale: float = 0.02) 
     return out
 
 
+def synthetic_model(seed: int, n_layers: int, d: int, f: int, vocab: int,
+                    scale: float = 0.02, tied_output: bool = False) -> dict:
+    """``synthetic.generate_synthetic_model`` (synthetic.py:46-61): one generator, draw
+    order tok_emb, then every layer's random_layer, then the untied head; norm
+    gains are ones."""
+    rng = np.random.default_rng(seed)
+    tok_emb = gaussian(rng, (vocab, d), scale)
+    layers = []
+    for _ in range(n_layers):
+        lw = random_layer(rng, d, f, scale)
+        lw["attn_norm"] = np.ones(d, F32)
+        lw["ffn_norm"] = np.ones(d, F32)
+        layers.append(lw)
+    w_out = None if tied_output else gaussian(rng, (d, vocab), scale)
+    return {"tok_emb": tok_emb, "layers": layers, "final_norm": np.ones(d, F32), "w_out": w_out}
+
+
 def init_predictor(rng: np.random.Generator, d: int, f: int, r: int | None = None,
                    scale: float = 0.02) -> dict:
     """Draw order query, w1, w2.  ``predictor.py:58-65``."""

@@ -41,6 +41,13 @@ SIGNATURES = {
     "ffwd_ffn_layer": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _vp, _vp, _vp,
                                 _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp,
                                 _vp, _vp, _vp, _c_int, _vp, _c_size, _vp]),
+    "ffwd_ffn_layer2": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _vp, _vp, _vp,
+                                 _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp,
+                                 _vp, _vp, _vp, _c_int, _vp, _vp, _vp, _c_size, _vp]),
+    "ffwd_rmsnorm": (_c_int, [_vp, _vp, _c_int, _c_int, ctypes.c_double, _vp, _vp, _vp, _vp,
+                              _c_int, _c_int, _vp]),
+    "ffwd_rope": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp,
+                           _c_int, _vp]),
     "ffwd_timing_enable": (_c_int, [_c_int]),
     "ffwd_timing_read": (_c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_c_int),
                                   _c_int]),

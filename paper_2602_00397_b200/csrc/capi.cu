@@ -129,11 +129,11 @@ Pred carve_pred(Carve& c, int nb, int d, int r, int f, bool with_scores) {
 
 int run_predictor(const void* x, bool x_is_f32, int T, int d, int b0, int nb, const float* query,
                   const float* w1, const float* w2, int r, int f, const Pred& p, float* scores,
-                  cudaStream_t s) {
+                  cudaStream_t s, const float* logits_in = nullptr) {
   const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));  // predictor.py:76
   {
     StageTimer tm(kPool, s);
-    FFWD_CUDA(launch_pool(x, x_is_f32, T, d, b0, nb, query, sqrt_d, p.logits, p.pooled, s),
+    FFWD_CUDA(launch_pool(x, x_is_f32, T, d, b0, nb, query, sqrt_d, p.logits, p.pooled, logits_in, s),
               "pool");
   }
   {
@@ -397,12 +397,13 @@ size_t ffwd_layer_workspace_bytes(int T, int d, int f_global, int f_local, int r
   return c.off;
 }
 
-int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t, const void* wd,
-                   int f_local, int rc_local, const float* query, const float* w1,
-                   const float* w2, int r, int f_global, int k, int dense_first_last,
-                   int has_comp, int tp_rank, int tp_size, float* y, const float* residual,
-                   void* x_next_bf16, int32_t* idx_global, int ld_idx_global, void* workspace,
-                   size_t workspace_bytes, void* stream) {
+int ffwd_ffn_layer2(const void* x_bf16, int T, int d, const void* wgu_t, const void* wd,
+                    int f_local, int rc_local, const float* query, const float* w1,
+                    const float* w2, int r, int f_global, int k, int dense_first_last,
+                    int has_comp, int tp_rank, int tp_size, float* y, const float* residual,
+                    void* x_next_bf16, int32_t* idx_global, int ld_idx_global,
+                    const float* x_pred_f32, const float* logits_in, void* workspace,
+                    size_t workspace_bytes, void* stream) {
   g_err.clear();
   int rc = check_common(T, d, f_global, k);
   if (rc) return rc;
@@ -428,7 +429,10 @@ int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t, const vo
   if (nb > 0) {
     if (d % 8 != 0) return fail(FFWD_ERR_UNSUPPORTED, "predictor needs d_model %% 8 == 0");
     if (idx_global && ld_idx_global < k) return fail(FFWD_ERR_VALIDATION, "ld_idx_global < k");
-    rc = run_predictor(x_bf16, false, T, d, b0, nb, query, w1, w2, r, f_global, p, p.scores, s);
+    rc = x_pred_f32 ? run_predictor(x_pred_f32, true, T, d, b0, nb, query, w1, w2, r, f_global,
+                                    p, p.scores, s, logits_in)
+                    : run_predictor(x_bf16, false, T, d, b0, nb, query, w1, w2, r, f_global, p,
+                                    p.scores, s, logits_in);
     if (rc) return rc;
     {
       StageTimer tm(kTopk, s);
@@ -439,6 +443,52 @@ int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t, const vo
   }
   return run_ffn(x_bf16, T, d, wgu_t, wd, f_local, rc_local, w, w.idx_local, w.ld_local, b0, nb,
                  tp_size > 1 ? w.counts : nullptr, k, 0, has_comp, y, residual, x_next_bf16, s);
+}
+
+int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t, const void* wd,
+                   int f_local, int rc_local, const float* query, const float* w1,
+                   const float* w2, int r, int f_global, int k, int dense_first_last,
+                   int has_comp, int tp_rank, int tp_size, float* y, const float* residual,
+                   void* x_next_bf16, int32_t* idx_global, int ld_idx_global, void* workspace,
+                   size_t workspace_bytes, void* stream) {
+  return ffwd_ffn_layer2(x_bf16, T, d, wgu_t, wd, f_local, rc_local, query, w1, w2, r, f_global,
+                         k, dense_first_last, has_comp, tp_rank, tp_size, y, residual,
+                         x_next_bf16, idx_global, ld_idx_global, nullptr, nullptr, workspace,
+                         workspace_bytes, stream);
+}
+
+int ffwd_rmsnorm(const float* x, const float* gain, int T, int d, double eps, void* out_bf16,
+                 float* out_f32, const float* query, float* logits, int logit_row0,
+                 int logit_row1, void* stream) {
+  g_err.clear();
+  if (T < 1 || d < 4 || d % 4 != 0)
+    return fail(FFWD_ERR_VALIDATION, "rmsnorm dims T=%d d=%d (d must be a positive multiple of 4)",
+                T, d);
+  if (d > 16384) return fail(FFWD_ERR_UNSUPPORTED, "rmsnorm supports d_model <= 16384, got %d", d);
+  if (!out_bf16 && !out_f32) return fail(FFWD_ERR_VALIDATION, "rmsnorm needs an output");
+  if (query && (!logits || logit_row0 < 0 || logit_row1 > T || logit_row0 > logit_row1))
+    return fail(FFWD_ERR_VALIDATION, "rmsnorm logit rows [%d, %d) outside [0, %d)", logit_row0,
+                logit_row1, T);
+  const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));  // predictor.py:76
+  FFWD_CUDA(launch_rmsnorm(x, gain, T, d, eps, out_bf16, out_f32, query, sqrt_d, logits,
+                           logit_row0, logit_row1, static_cast<cudaStream_t>(stream)),
+            "rmsnorm");
+  return FFWD_OK;
+}
+
+int ffwd_rope(void* qk, int is_f32, int T, int row_stride, int k_col, int n_heads, int d_head,
+              const double* cos_t, const double* sin_t, int pos0, void* stream) {
+  g_err.clear();
+  if (T < 1 || n_heads < 1 || d_head < 2 || d_head % 2 != 0)
+    return fail(FFWD_ERR_VALIDATION, "rope dims T=%d heads=%d d_head=%d", T, n_heads, d_head);
+  if (k_col < n_heads * d_head || row_stride < k_col + n_heads * d_head)
+    return fail(FFWD_ERR_VALIDATION, "rope layout: row_stride=%d k_col=%d for %d x %d", row_stride,
+                k_col, n_heads, d_head);
+  if (pos0 < 0) return fail(FFWD_ERR_VALIDATION, "rope pos0=%d < 0", pos0);
+  FFWD_CUDA(launch_rope(qk, is_f32 != 0, T, row_stride, k_col, n_heads, d_head, cos_t, sin_t,
+                        pos0, static_cast<cudaStream_t>(stream)),
+            "rope");
+  return FFWD_OK;
 }
 
 int ffwd_timing_enable(int on) {

@@ -44,7 +44,14 @@ struct PlanCounts {
 // partials reduced in fixed order).  `logits`: blk_count * 128 floats of scratch.
 cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begin,
                         int blk_count, const float* query, float sqrt_d, float* logits,
-                        float* pooled, cudaStream_t s);
+                        float* pooled, const float* logits_in, cudaStream_t s);
+// FFN-input producers of the full prefill (norm.cu).
+cudaError_t launch_rmsnorm(const float* x, const float* gain, int T, int d, double eps,
+                           void* out_bf16, float* out_f32, const float* query, float sqrt_d,
+                           float* logits, int logit_row0, int logit_row1, cudaStream_t s);
+cudaError_t launch_rope(void* qk, bool is_f32, int T, int row_stride, int k_col, int n_heads,
+                        int d_head, const double* cos_t, const double* sin_t, int pos0,
+                        cudaStream_t s);
 // `partial` (nullable, gemm_f64acc_partial_bytes) enables split-K.
 size_t gemm_f64acc_partial_bytes(int M, int K, int N);
 cudaError_t launch_gemm_f64acc(const float* A, const float* B, float* C, int M, int K, int N,

@@ -1,0 +1,180 @@
+// Producers of the FFN input on the full-prefill (TTFT) path, engine.py:262-267.
+//
+//   rmsnorm_kernel  out = f32(x * (1 / sqrt(mean_f64(x^2) + eps)) * gain), all in f64
+//                   like kernels.rmsnorm (kernels.py:96-106), written as bf16 (the
+//                   FFN / attention GEMM operand) and optionally as f32.  When a
+//                   predictor query is given it also emits the predictor logits of
+//                   the row (predictor.py:76: f32(q . x) / f32(sqrt d), f64
+//                   accumulation) from the bf16 values it just wrote, so the
+//                   predictor's first pass over X disappears.
+//   rope_kernel     rotary embedding of Q and K in place (engine.py:50-68 apply_rope):
+//                   each head's (first half, second half) pairs rotated by the
+//                   position angle, products in f64 from an f64 cos/sin table, one
+//                   rounding to the storage type.
+//
+// Both are HBM bound: RMSNorm reads 4 B and writes 2 (+4) B per element, RoPE reads
+// and writes Q and K once.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "ffwd_internal.h"
+
+namespace ffwd {
+
+namespace {
+
+constexpr int kNormThreads = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Sum over the CTA in warp order (fixed, deterministic).
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  v = warp_sum(v);
+  __syncthreads();  // `red` may still be read from a previous call
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < kNormThreads / 32; ++w) s += red[w];
+  return s;
+}
+
+// One CTA per row; thread i owns the float4 groups {i + 256 j}, held in registers
+// between the two passes.  kMaxV = float4 groups per thread (d <= 1024 * kMaxV).
+template <int kMaxV>
+__global__ void __launch_bounds__(kNormThreads)
+    rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ gain, int d,
+                   double eps, __nv_bfloat16* __restrict__ out_bf16, float* __restrict__ out_f32,
+                   const float* __restrict__ query, float sqrt_d, float* __restrict__ logits,
+                   int logit_row0, int logit_row1) {
+  __shared__ double red[kNormThreads / 32];
+  const int row = blockIdx.x;
+  const int nv = d / 4;
+  const float4* xr = reinterpret_cast<const float4*>(x + static_cast<size_t>(row) * d);
+  float4 v[kMaxV];
+  double ss = 0.0;
+#pragma unroll
+  for (int j = 0; j < kMaxV; ++j) {
+    const int g = threadIdx.x + kNormThreads * j;
+    v[j] = g < nv ? __ldg(xr + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const double a = v[j].x, b = v[j].y, c = v[j].z, e = v[j].w;
+    ss += (a * a + b * b) + (c * c + e * e);
+  }
+  const double mean = block_sum(ss, red) / static_cast<double>(d);
+  const double scale = 1.0 / sqrt(mean + eps);  // kernels.py:105
+  const bool want_logit = query != nullptr && row >= logit_row0 && row < logit_row1;
+  double z = 0.0;
+  const float4* gr = reinterpret_cast<const float4*>(gain);
+  const float4* qr = reinterpret_cast<const float4*>(query);
+#pragma unroll
+  for (int j = 0; j < kMaxV; ++j) {
+    const int g = threadIdx.x + kNormThreads * j;
+    if (g >= nv) continue;
+    const float4 w = __ldg(gr + g);
+    float4 o;
+    o.x = static_cast<float>(__dmul_rn(__dmul_rn(v[j].x, scale), w.x));
+    o.y = static_cast<float>(__dmul_rn(__dmul_rn(v[j].y, scale), w.y));
+    o.z = static_cast<float>(__dmul_rn(__dmul_rn(v[j].z, scale), w.z));
+    o.w = static_cast<float>(__dmul_rn(__dmul_rn(v[j].w, scale), w.w));
+    const size_t off = static_cast<size_t>(row) * d + 4 * static_cast<size_t>(g);
+    if (out_f32) reinterpret_cast<float4*>(out_f32 + off)[0] = o;
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y);
+    const __nv_bfloat162 hi = __floats2bfloat162_rn(o.z, o.w);
+    if (out_bf16) {
+      uint2 pk;
+      pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(out_bf16 + off)[0] = pk;
+    }
+    if (want_logit) {  // q . bf16(x), the operand the pooling pass would read
+      const float4 q = __ldg(qr + g);
+      const float2 l2 = __bfloat1622float2(lo), h2 = __bfloat1622float2(hi);
+      z = fma(static_cast<double>(q.x), static_cast<double>(l2.x), z);
+      z = fma(static_cast<double>(q.y), static_cast<double>(l2.y), z);
+      z = fma(static_cast<double>(q.z), static_cast<double>(h2.x), z);
+      z = fma(static_cast<double>(q.w), static_cast<double>(h2.y), z);
+    }
+  }
+  if (query != nullptr && row >= logit_row0 && row < logit_row1) {
+    const double zs = block_sum(z, red);
+    if (threadIdx.x == 0)
+      logits[row - logit_row0] = __fdiv_rn(static_cast<float>(zs), sqrt_d);  // predictor.py:76
+  }
+}
+
+// grid (T, 2 * n_heads): blockIdx.y < n_heads rotates Q head y, else K head y - n_heads.
+// The (T, row_stride) buffer holds Q at column 0 and K at column k_col.
+template <typename E>
+__global__ void rope_kernel(E* __restrict__ qk, int row_stride, int k_col, int n_heads,
+                            int d_head, const double* __restrict__ cos_t,
+                            const double* __restrict__ sin_t, int pos0) {
+  const int t = blockIdx.x;
+  const int y = blockIdx.y;
+  const int half = d_head / 2;
+  const int col0 = (y < n_heads ? 0 : k_col) + (y % n_heads) * d_head;
+  E* p = qk + static_cast<size_t>(t) * row_stride + col0;
+  const double* ct = cos_t + static_cast<size_t>(pos0 + t) * half;
+  const double* st = sin_t + static_cast<size_t>(pos0 + t) * half;
+  for (int i = threadIdx.x; i < half; i += blockDim.x) {
+    const double x1 = static_cast<double>(static_cast<float>(p[i]));
+    const double x2 = static_cast<double>(static_cast<float>(p[half + i]));
+    const double c = ct[i], s = st[i];
+    // engine.py:65-66, each f64 product and sum rounded separately (no contraction)
+    const float o1 = static_cast<float>(__dsub_rn(__dmul_rn(x1, c), __dmul_rn(x2, s)));
+    const float o2 = static_cast<float>(__dadd_rn(__dmul_rn(x1, s), __dmul_rn(x2, c)));
+    if constexpr (std::is_same_v<E, float>) {
+      p[i] = o1;
+      p[half + i] = o2;
+    } else {
+      p[i] = __float2bfloat16_rn(o1);
+      p[half + i] = __float2bfloat16_rn(o2);
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_rmsnorm(const float* x, const float* gain, int T, int d, double eps,
+                           void* out_bf16, float* out_f32, const float* query, float sqrt_d,
+                           float* logits, int logit_row0, int logit_row1, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  const int nv = (d / 4 + kNormThreads - 1) / kNormThreads;
+  auto* ob = static_cast<__nv_bfloat16*>(out_bf16);
+#define FFWD_NORM(V)                                                                      \
+  rmsnorm_kernel<V><<<T, kNormThreads, 0, s>>>(x, gain, d, eps, ob, out_f32, query, sqrt_d, \
+                                               logits, logit_row0, logit_row1)
+  if (nv <= 1) FFWD_NORM(1);
+  else if (nv <= 2) FFWD_NORM(2);
+  else if (nv <= 4) FFWD_NORM(4);
+  else if (nv <= 8) FFWD_NORM(8);
+  else if (nv <= 16) FFWD_NORM(16);
+  else return cudaErrorInvalidValue;
+#undef FFWD_NORM
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rope(void* qk, bool is_f32, int T, int row_stride, int k_col, int n_heads,
+                        int d_head, const double* cos_t, const double* sin_t, int pos0,
+                        cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  const dim3 grid(T, 2 * n_heads);
+  const int threads = d_head / 2 < 32 ? 32 : (d_head / 2 > 128 ? 128 : d_head / 2);
+  if (is_f32)
+    rope_kernel<float><<<grid, threads, 0, s>>>(static_cast<float*>(qk), row_stride, k_col,
+                                                n_heads, d_head, cos_t, sin_t, pos0);
+  else
+    rope_kernel<__nv_bfloat16><<<grid, threads, 0, s>>>(static_cast<__nv_bfloat16*>(qk),
+                                                        row_stride, k_col, n_heads, d_head,
+                                                        cos_t, sin_t, pos0);
+  return cudaGetLastError();
+}
+
+}  // namespace ffwd

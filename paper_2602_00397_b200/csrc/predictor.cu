@@ -343,19 +343,23 @@ int gemm_splits(int M, int K, int N) {
 
 cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begin, int blk_count,
                         const float* query, float sqrt_d, float* logits, float* pooled,
-                        cudaStream_t s) {
+                        const float* logits_in, cudaStream_t s) {
   if (blk_count <= 0) return cudaSuccess;
   const int tok0 = blk_begin * kBlockTokens;
   const int ntok = std::min(T, (blk_begin + blk_count) * kBlockTokens) - tok0;
   const dim3 g1((ntok + kLogitWarps - 1) / kLogitWarps);
   const dim3 g2((d + kPoolCols - 1) / kPoolCols, blk_count);
+  // logits_in: precomputed by the producer of X (absolute token index), e.g. the fused
+  // RMSNorm; the first pass is then skipped.
+  const float* lg = logits_in ? logits_in + tok0 : logits;
   if (x_is_f32) {
-    logits_kernel<true><<<g1, kLogitThreads, 0, s>>>(x, d, tok0, ntok, query, sqrt_d, logits);
-    pooled_kernel<true><<<g2, kPoolThreads, 0, s>>>(x, T, d, blk_begin, blk_count, logits, pooled);
+    if (!logits_in)
+      logits_kernel<true><<<g1, kLogitThreads, 0, s>>>(x, d, tok0, ntok, query, sqrt_d, logits);
+    pooled_kernel<true><<<g2, kPoolThreads, 0, s>>>(x, T, d, blk_begin, blk_count, lg, pooled);
   } else {
-    logits_kernel<false><<<g1, kLogitThreads, 0, s>>>(x, d, tok0, ntok, query, sqrt_d, logits);
-    pooled_kernel<false><<<g2, kPoolThreads, 0, s>>>(x, T, d, blk_begin, blk_count, logits,
-                                                     pooled);
+    if (!logits_in)
+      logits_kernel<false><<<g1, kLogitThreads, 0, s>>>(x, d, tok0, ntok, query, sqrt_d, logits);
+    pooled_kernel<false><<<g2, kPoolThreads, 0, s>>>(x, T, d, blk_begin, blk_count, lg, pooled);
   }
   return cudaGetLastError();
 }

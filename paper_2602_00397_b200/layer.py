@@ -176,7 +176,9 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
                      dense_first_last: bool = True, has_comp: bool = True,
                      out: torch.Tensor | None = None, return_indices: bool = False,
                      workspace: torch.Tensor | None = None,
-                     residual: torch.Tensor | None = None, x_next: torch.Tensor | None = None):
+                     residual: torch.Tensor | None = None, x_next: torch.Tensor | None = None,
+                     x_pred_f32: torch.Tensor | None = None,
+                     logits_in: torch.Tensor | None = None):
     """One layer's FFN branch over every block of x (T, d); returns y (T, d) f32.
 
     Semantics of ``engine.py:254-310`` (mode "predicted"): blocks 0 and n-1 run
@@ -188,6 +190,10 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
     ``residual`` (f32 (T, d), may be ``out``) fuses the residual add of
     ``engine.py:308`` into the down-projection epilogue; ``x_next`` (bf16 (T, d))
     receives bf16(y) as the next layer's input (tp_size == 1 only).
+    ``x_pred_f32`` (f32 (T, d)) makes the predictor pool over f32 inputs (the
+    reference's f32 RMSNorm output) instead of x; ``logits_in`` (f32 (T,)) are
+    per-token predictor logits already produced by the FFN-input producer
+    (``norm.rmsnorm(..., predictor=...)``), which skips the pooling's first pass.
     """
     dev = packed.device
     xb = _x_bf16(x, dev)
@@ -212,12 +218,18 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
     ws_n = layer_workspace_bytes(T, packed, predictor.r, k, dense_first_last)
     ws = workspace if workspace is not None and workspace.numel() >= ws_n else \
         _dev.workspace(dev, ws_n)
-    _lib.check(lib.ffwd_ffn_layer(
+    for name, t, shape, dt in (("x_pred_f32", x_pred_f32, (T, d), torch.float32),
+                               ("logits_in", logits_in, (T,), torch.float32)):
+        if t is not None and (not t.is_cuda or t.dtype != dt or tuple(t.shape) != shape
+                              or not t.is_contiguous()):
+            raise ValidationError(f"{name} must be a contiguous CUDA {dt} tensor of shape {shape}")
+    _lib.check(lib.ffwd_ffn_layer2(
         xb.data_ptr(), T, d, packed.wgu_t.data_ptr(), packed.wd.data_ptr(), packed.f_local,
         packed.rc_local, predictor.query.data_ptr(), predictor.w1.data_ptr(),
         predictor.w2.data_ptr(), predictor.r, predictor.f, k, int(dense_first_last),
         int(has_comp and packed.rc_local > 0), packed.tp_rank, packed.tp_size, y.data_ptr(),
-        _dev.ptr(residual), _dev.ptr(x_next), _dev.ptr(idx), k if idx is not None else 0, ws.data_ptr(), ws.numel(),
+        _dev.ptr(residual), _dev.ptr(x_next), _dev.ptr(idx), k if idx is not None else 0,
+        _dev.ptr(x_pred_f32), _dev.ptr(logits_in), ws.data_ptr(), ws.numel(),
         _dev.stream_handle(dev)), "ffn_layer")
     if return_indices:
         return y, idx

@@ -60,3 +60,31 @@ def load_case(name: str, check_sha: bool = True) -> dict:
     g.update(x=x, lw=lw, pred=pred, comp=comp, d=d, f=f, T=T, k=int(g["k"]),
              dense_first_last=bool(int(g["dense_first_last"])))
     return g
+
+
+def load_prefill_case(name: str = "prefill_small") -> dict:
+    """Regenerate the golden full-prefill case (make_golden.make_prefill_case) with the
+    oracle and check every input against the reference's digests."""
+    g = golden(name)
+    seed, L, d, f, V, T = (int(g[k]) for k in ("seed", "n_layers", "d", "f", "vocab", "T"))
+    m = orc.synthetic_model(seed, L, d, f, V)
+    for lw in m["layers"]:
+        for kk in ("w_gate", "w_up", "w_down"):
+            lw[kk] = orc.bf16_round(lw[kk])
+    preds = [orc.init_predictor(np.random.default_rng([seed, l]), d, f) for l in range(L)]
+    comps = [{k: orc.bf16_round(v) for k, v in
+              orc.init_compensator(np.random.default_rng([seed + 1, l]), d).items()}
+             for l in range(L)]
+    tokens = np.random.default_rng([seed, 5]).integers(0, V, T)
+    digests = {
+        "sha_model": sha(m["tok_emb"], m["w_out"], *[lw[n] for lw in m["layers"] for n in
+                                                      ("wq", "wk", "wv", "wo", "w_gate", "w_up",
+                                                       "w_down")]),
+        "sha_pred": sha(*[a for p in preds for a in (p["query"], p["w1"], p["w2"])]),
+        "sha_comp": sha(*[a for c in comps for a in (c["w1"], c["w2"])]),
+        "sha_tokens": sha(tokens),
+    }
+    for k, v in digests.items():
+        if str(g[k]) != v:
+            raise AssertionError(f"{name}: regenerated {k} differs from the reference's inputs")
+    return dict(golden=g, model=m, preds=preds, comps=comps, tokens=tokens)

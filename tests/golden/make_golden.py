@@ -177,7 +177,53 @@ def make_scheduler():
     print(f"scheduler: {len(S)} allocations")
 
 
+def make_prefill_case(name="prefill_small", seed=2026, n_layers=2, d=256, f=768, n_heads=4,
+                      vocab=512, T=512, budget=0.5):
+    """Full block-wise prefill (engine.prefill_blockwise, predicted mode, and
+    prefill_dense) on a synthetic model; FFN and compensator weights bf16-rounded."""
+    from sparseprefill.engine import prefill_blockwise, prefill_dense
+    from sparseprefill.scheduler import uniform_plan
+    from sparseprefill.synthetic import generate_synthetic_model
+    cfg = ModelConfig(n_layers=n_layers, d_model=d, d_ffn=f, n_heads=n_heads, vocab_size=vocab,
+                      block_size=128, max_context=T)
+    w = generate_synthetic_model(cfg, seed)
+    for lw in w.layers:
+        lw.w_gate, lw.w_up, lw.w_down = (bf16_round(lw.w_gate), bf16_round(lw.w_up),
+                                         bf16_round(lw.w_down))
+    preds = [init_predictor(cfg, np.random.default_rng([seed, l])) for l in range(n_layers)]
+    comps = []
+    for l in range(n_layers):
+        c = init_compensator(cfg, np.random.default_rng([seed + 1, l]))
+        c.w1, c.w2 = bf16_round(c.w1), bf16_round(c.w2)
+        comps.append(c)
+    tokens = np.random.default_rng([seed, 5]).integers(0, vocab, T)
+    plan = uniform_plan(n_layers, budget)
+    res = prefill_blockwise(w, tokens, plan, mode="predicted", predictors=preds,
+                            compensators=comps, keep_masks=True)
+    dense = prefill_dense(w, tokens)
+    keys = sorted(res.masks)
+    out = dict(seed=seed, n_layers=n_layers, d=d, f=f, n_heads=n_heads, vocab=vocab, T=T,
+               budget=budget, k=budget_to_k(budget, f),
+               mask_keys=np.array(keys, np.int32),
+               masks=np.stack([res.masks[kk].indices.astype(np.int32) for kk in keys]),
+               hidden_rows=np.arange(0, T, 4), hidden=res.hidden[::4].astype(np.float32),
+               last_logits=res.last_logits, dense_hidden=dense.hidden[::4].astype(np.float32),
+               dense_last_logits=dense.last_logits,
+               flops_total=np.int64(res.flops.total()),
+               sha_model=sha(w.tok_emb, w.w_out, *[getattr(lw, n) for lw in w.layers for n in
+                                                    ("wq", "wk", "wv", "wo", "w_gate", "w_up",
+                                                     "w_down")]),
+               sha_pred=sha(*[a for p in preds for a in (p.query, p.w1, p.w2)]),
+               sha_comp=sha(*[a for c in comps for a in (c.w1, c.w2)]),
+               sha_tokens=sha(tokens))
+    np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **out)
+    print(f"{name}: {len(keys)} masks, flops {res.flops.total()}")
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "prefill":
+        make_prefill_case()
+        sys.exit(0)
     make_topk_edges()
     make_scheduler()
     # tiny, with a short final block (300 = 128 + 128 + 44)
@@ -196,3 +242,4 @@ if __name__ == "__main__":
               dense_first_last=False)
     make_case("qwen8b_pred", d=4096, f=12288, T=384, seed=9, with_ffn=False,
               dense_first_last=False, budget=0.37)
+    make_prefill_case()
