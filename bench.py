@@ -268,6 +268,63 @@ def run_reference(args, rank: int, world: int) -> None:
     print(json.dumps(out), flush=True)
 
 
+# ------------------------------------------------------------------ TTFT
+VOCAB = 128256  # Llama-3 vocabulary (embedding + head of the TTFT model)
+
+
+def measure_ttft(layers, cfg_name: str, dev, steps: int) -> dict:
+    """Time-to-first-token of the full prefill (engine.prefill_blockwise semantics,
+    prefill.py): embedding, 32 x (RMSNorm, QKV, RoPE, causal SDPA, Wo, RMSNorm +
+    predictor logits, FFN hot path with residual), final norm and head, for the
+    predicted (50%) and dense modes.  The reference architecture (model.py:18-84:
+    multi-head attention, d x d Wq/Wk/Wv/Wo, head_dim 128 here) with random-init
+    weights; the FFN layers are the bench's own.  Timed from host token ids to host
+    last-token logits (H2D / D2H inside the region), CUDA events, mean of `steps`."""
+    import paper_2602_00397_b200 as ff
+    from paper_2602_00397_b200.prefill import DeviceLayer, DeviceModel, prefill
+    d, f, L, T, keep = CONFIGS[cfg_name]
+    cfg = ff.ModelConfig(n_layers=L, d_model=d, d_ffn=f, n_heads=d // 128, vocab_size=VOCAB,
+                         max_context=T)
+    g = torch.Generator(device=dev)
+    g.manual_seed(4242)
+
+    def w(*shape, dt=torch.bfloat16):
+        return torch.randn(shape, generator=g, device=dev, dtype=torch.float32).mul_(0.02).to(dt)
+
+    ones = torch.ones(d, device=dev)
+    dls = [DeviceLayer(wqkv_t=w(3 * d, d), wo_t=w(d, d), attn_norm=ones, ffn_norm=ones,
+                       ffn=packed, predictor=dp, k=k) for packed, dp, k in layers]
+    model = DeviceModel(config=cfg, tok_emb=w(VOCAB, d, dt=torch.float32), layers=dls,
+                        final_norm=ones, head=w(d, VOCAB, dt=torch.float32),
+                        dense_first_last=True, attn_dtype=torch.bfloat16, has_comp=True)
+    tokens = np.random.default_rng(7).integers(0, VOCAB, T)
+    out = {}
+    for mode in ("predicted", "dense", "predicted", "dense"):  # warm-up (cuDNN plans, pools)
+        prefill(model, tokens, mode=mode).last_logits.cpu()
+    for mode in ("predicted", "dense"):
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            res = prefill(model, tokens, mode=mode)
+            res.last_logits.cpu()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / steps
+        out[mode] = {"ms": ms, "flops": int(res.flops.total()),
+                     "effective_tflops": res.flops.total() / (ms * 1e-3) / 1e12}
+    del model, dls
+    torch.cuda.empty_cache()
+    return {"unit": "ms", "T": T, "layers": L, "n_heads": cfg.n_heads, "vocab": VOCAB,
+            "predicted_50pct_ms": out["predicted"]["ms"], "dense_ms": out["dense"]["ms"],
+            "speedup_vs_dense": out["dense"]["ms"] / out["predicted"]["ms"],
+            "predicted_effective_tflops": out["predicted"]["effective_tflops"],
+            "dense_effective_tflops": out["dense"]["effective_tflops"],
+            "attention": "torch SDPA (cuDNN/flash, bf16), QKV/O projections cuBLAS bf16",
+            "timed": "host token ids -> host last-token logits, CUDA events, mean of "
+                     f"{steps} prefills after 2 warm-up prefills per mode"}
+
+
 # ------------------------------------------------------------------ GPU arm
 def run_gpu(args, rank: int, world: int) -> None:
     import paper_2602_00397_b200 as ff
@@ -422,6 +479,9 @@ def run_gpu(args, rank: int, world: int) -> None:
                         "speedup_vs_cublas_dense": cub / value,
                         "speedup_vs_own_dense": own_dense / value,
                         "dense_tflops_cublas": 6 * T * d * f / (cub * 1e-3) / 1e12}
+    # ---- TTFT of the full prefill (rank 0, single GPU)
+    if world == 1 and not args.skip_ttft:
+        out["ttft"] = measure_ttft(layers, args.config, dev, max(1, min(3, args.steps)))
     del layers
     torch.cuda.empty_cache()
 
@@ -448,6 +508,7 @@ def main():
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug)")
     ap.add_argument("--skip-dense", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-ttft", action="store_true")
     ap.add_argument("--raster", default="", help="UP,DOWN blocks per L2 raster group (tuning)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

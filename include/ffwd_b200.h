@@ -149,15 +149,18 @@ FFWD_API int ffwd_ffn_layer2(const void* x_bf16, int T, int d, const void* wgu_t
 /*
  * kernels.rmsnorm (kernels.py:96-106) of the f32 residual stream x [T x d]:
  * out = f32(x / sqrt(mean_f64(x^2) + eps) * gain), evaluated in f64 like the
- * reference, written to out_bf16 (bf16 [T x d]) and/or out_f32.  With a
+ * reference, written to out_bf16 (bf16 [T x d]) and/or out_f32.  With `add`
+ * ([T x d], f32 when add_kind == 1, bf16 when 2) the residual add x += add
+ * (engine.py:265, the attention output) runs first and x is updated in place.  With a
  * predictor `query` (f32 [d]) it also writes logits[t - logit_row0] =
  * f32(q . bf16(out_t)) / f32(sqrt d) for rows t in [logit_row0, logit_row1):
  * the FFN-input producer fused with the predictor's first pass (engine.py:267
  * followed by predictor.py:76).  d % 4 == 0, d <= 16384.
  */
-FFWD_API int ffwd_rmsnorm(const float* x, const float* gain, int T, int d, double eps,
-                          void* out_bf16, float* out_f32, const float* query, float* logits,
-                          int logit_row0, int logit_row1, void* stream);
+FFWD_API int ffwd_rmsnorm(float* x, const float* gain, int T, int d, double eps,
+                          const void* add, int add_kind, void* out_bf16, float* out_f32,
+                          const float* query, float* logits, int logit_row0, int logit_row1,
+                          void* stream);
 
 /*
  * apply_rope (engine.py:50-68) in place on Q and K of one [T x row_stride]

@@ -44,8 +44,8 @@ SIGNATURES = {
     "ffwd_ffn_layer2": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _vp, _vp, _vp,
                                  _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp,
                                  _vp, _vp, _vp, _c_int, _vp, _vp, _vp, _c_size, _vp]),
-    "ffwd_rmsnorm": (_c_int, [_vp, _vp, _c_int, _c_int, ctypes.c_double, _vp, _vp, _vp, _vp,
-                              _c_int, _c_int, _vp]),
+    "ffwd_rmsnorm": (_c_int, [_vp, _vp, _c_int, _c_int, ctypes.c_double, _vp, _c_int, _vp, _vp,
+                              _vp, _vp, _c_int, _c_int, _vp]),
     "ffwd_rope": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp,
                            _c_int, _vp]),
     "ffwd_timing_enable": (_c_int, [_c_int]),

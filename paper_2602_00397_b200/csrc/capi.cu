@@ -457,21 +457,24 @@ int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t, const vo
                          workspace_bytes, stream);
 }
 
-int ffwd_rmsnorm(const float* x, const float* gain, int T, int d, double eps, void* out_bf16,
-                 float* out_f32, const float* query, float* logits, int logit_row0,
-                 int logit_row1, void* stream) {
+int ffwd_rmsnorm(float* x, const float* gain, int T, int d, double eps, const void* add,
+                 int add_kind, void* out_bf16, float* out_f32, const float* query, float* logits,
+                 int logit_row0, int logit_row1, void* stream) {
   g_err.clear();
   if (T < 1 || d < 4 || d % 4 != 0)
     return fail(FFWD_ERR_VALIDATION, "rmsnorm dims T=%d d=%d (d must be a positive multiple of 4)",
                 T, d);
   if (d > 16384) return fail(FFWD_ERR_UNSUPPORTED, "rmsnorm supports d_model <= 16384, got %d", d);
   if (!out_bf16 && !out_f32) return fail(FFWD_ERR_VALIDATION, "rmsnorm needs an output");
+  if (add && (add_kind < 1 || add_kind > 2))
+    return fail(FFWD_ERR_VALIDATION, "rmsnorm add_kind must be 1 (f32) or 2 (bf16)");
   if (query && (!logits || logit_row0 < 0 || logit_row1 > T || logit_row0 > logit_row1))
     return fail(FFWD_ERR_VALIDATION, "rmsnorm logit rows [%d, %d) outside [0, %d)", logit_row0,
                 logit_row1, T);
   const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));  // predictor.py:76
-  FFWD_CUDA(launch_rmsnorm(x, gain, T, d, eps, out_bf16, out_f32, query, sqrt_d, logits,
-                           logit_row0, logit_row1, static_cast<cudaStream_t>(stream)),
+  FFWD_CUDA(launch_rmsnorm(x, gain, T, d, eps, add, add ? add_kind : 0, out_bf16, out_f32, query,
+                           sqrt_d, logits, logit_row0, logit_row1,
+                           static_cast<cudaStream_t>(stream)),
             "rmsnorm");
   return FFWD_OK;
 }
@@ -479,8 +482,9 @@ int ffwd_rmsnorm(const float* x, const float* gain, int T, int d, double eps, vo
 int ffwd_rope(void* qk, int is_f32, int T, int row_stride, int k_col, int n_heads, int d_head,
               const double* cos_t, const double* sin_t, int pos0, void* stream) {
   g_err.clear();
-  if (T < 1 || n_heads < 1 || d_head < 2 || d_head % 2 != 0)
-    return fail(FFWD_ERR_VALIDATION, "rope dims T=%d heads=%d d_head=%d", T, n_heads, d_head);
+  if (T < 1 || n_heads < 1 || d_head < 4 || d_head % 4 != 0)
+    return fail(FFWD_ERR_VALIDATION, "rope dims T=%d heads=%d d_head=%d (d_head %% 4 == 0)", T,
+                n_heads, d_head);
   if (k_col < n_heads * d_head || row_stride < k_col + n_heads * d_head)
     return fail(FFWD_ERR_VALIDATION, "rope layout: row_stride=%d k_col=%d for %d x %d", row_stride,
                 k_col, n_heads, d_head);

@@ -46,9 +46,10 @@ cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begi
                         int blk_count, const float* query, float sqrt_d, float* logits,
                         float* pooled, const float* logits_in, cudaStream_t s);
 // FFN-input producers of the full prefill (norm.cu).
-cudaError_t launch_rmsnorm(const float* x, const float* gain, int T, int d, double eps,
-                           void* out_bf16, float* out_f32, const float* query, float sqrt_d,
-                           float* logits, int logit_row0, int logit_row1, cudaStream_t s);
+cudaError_t launch_rmsnorm(float* x, const float* gain, int T, int d, double eps,
+                           const void* add, int add_kind, void* out_bf16, float* out_f32,
+                           const float* query, float sqrt_d, float* logits, int logit_row0,
+                           int logit_row1, cudaStream_t s);
 cudaError_t launch_rope(void* qk, bool is_f32, int T, int row_stride, int k_col, int n_heads,
                         int d_head, const double* cos_t, const double* sin_t, int pos0,
                         cudaStream_t s);

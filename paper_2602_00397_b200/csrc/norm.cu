@@ -1,6 +1,7 @@
 // Producers of the FFN input on the full-prefill (TTFT) path, engine.py:262-267.
 //
-//   rmsnorm_kernel  out = f32(x * (1 / sqrt(mean_f64(x^2) + eps)) * gain), all in f64
+//   rmsnorm_kernel  [x += add, the residual add] then
+//                   out = f32(x * (1 / sqrt(mean_f64(x^2) + eps)) * gain), all in f64
 //                   like kernels.rmsnorm (kernels.py:96-106), written as bf16 (the
 //                   FFN / attention GEMM operand) and optionally as f32.  When a
 //                   predictor query is given it also emits the predictor logits of
@@ -49,22 +50,41 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 
 // One CTA per row; thread i owns the float4 groups {i + 256 j}, held in registers
 // between the two passes.  kMaxV = float4 groups per thread (d <= 1024 * kMaxV).
-template <int kMaxV>
+// kAdd: 0 none, 1 f32, 2 bf16 -- the residual add x += add (engine.py:265) fused in
+// front of the norm; the updated x is written back.
+template <int kMaxV, int kAdd>
 __global__ void __launch_bounds__(kNormThreads)
-    rmsnorm_kernel(const float* __restrict__ x, const float* __restrict__ gain, int d,
-                   double eps, __nv_bfloat16* __restrict__ out_bf16, float* __restrict__ out_f32,
-                   const float* __restrict__ query, float sqrt_d, float* __restrict__ logits,
-                   int logit_row0, int logit_row1) {
+    rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ gain, int d, double eps,
+                   const void* __restrict__ add, __nv_bfloat16* __restrict__ out_bf16,
+                   float* __restrict__ out_f32, const float* __restrict__ query, float sqrt_d,
+                   float* __restrict__ logits, int logit_row0, int logit_row1) {
   __shared__ double red[kNormThreads / 32];
   const int row = blockIdx.x;
   const int nv = d / 4;
-  const float4* xr = reinterpret_cast<const float4*>(x + static_cast<size_t>(row) * d);
+  float4* xr = reinterpret_cast<float4*>(x + static_cast<size_t>(row) * d);
   float4 v[kMaxV];
   double ss = 0.0;
 #pragma unroll
   for (int j = 0; j < kMaxV; ++j) {
     const int g = threadIdx.x + kNormThreads * j;
-    v[j] = g < nv ? __ldg(xr + g) : make_float4(0.f, 0.f, 0.f, 0.f);
+    v[j] = g < nv ? xr[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (kAdd != 0 && g < nv) {
+      float4 a4;
+      if constexpr (kAdd == 1) {
+        a4 = __ldg(reinterpret_cast<const float4*>(add) + static_cast<size_t>(row) * nv + g);
+      } else {
+        const uint2 raw =
+            __ldg(reinterpret_cast<const uint2*>(add) + static_cast<size_t>(row) * nv + g);
+        const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+        const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+        a4 = make_float4(lo.x, lo.y, hi.x, hi.y);
+      }
+      v[j].x = __fadd_rn(v[j].x, a4.x);
+      v[j].y = __fadd_rn(v[j].y, a4.y);
+      v[j].z = __fadd_rn(v[j].z, a4.z);
+      v[j].w = __fadd_rn(v[j].w, a4.w);
+      xr[g] = v[j];
+    }
     const double a = v[j].x, b = v[j].y, c = v[j].z, e = v[j].w;
     ss += (a * a + b * b) + (c * c + e * e);
   }
@@ -110,47 +130,63 @@ __global__ void __launch_bounds__(kNormThreads)
   }
 }
 
-// grid (T, 2 * n_heads): blockIdx.y < n_heads rotates Q head y, else K head y - n_heads.
-// The (T, row_stride) buffer holds Q at column 0 and K at column k_col.
+// One CTA per token; a thread rotates 2 consecutive pairs (i, i+1) of one head at a
+// time (vector loads of both halves).  Q heads at column 0, K heads at k_col.
 template <typename E>
-__global__ void rope_kernel(E* __restrict__ qk, int row_stride, int k_col, int n_heads,
-                            int d_head, const double* __restrict__ cos_t,
-                            const double* __restrict__ sin_t, int pos0) {
+__global__ void __launch_bounds__(256)
+    rope_kernel(E* __restrict__ qk, int row_stride, int k_col, int n_heads, int d_head,
+                const double* __restrict__ cos_t, const double* __restrict__ sin_t, int pos0) {
+  using E2 = std::conditional_t<std::is_same_v<E, float>, float2, __nv_bfloat162>;
   const int t = blockIdx.x;
-  const int y = blockIdx.y;
   const int half = d_head / 2;
-  const int col0 = (y < n_heads ? 0 : k_col) + (y % n_heads) * d_head;
-  E* p = qk + static_cast<size_t>(t) * row_stride + col0;
+  const int hu = half / 2;                 // 2-pair units per head
+  const int units = 2 * n_heads * hu;      // Q and K
+  E* rowp = qk + static_cast<size_t>(t) * row_stride;
   const double* ct = cos_t + static_cast<size_t>(pos0 + t) * half;
   const double* st = sin_t + static_cast<size_t>(pos0 + t) * half;
-  for (int i = threadIdx.x; i < half; i += blockDim.x) {
-    const double x1 = static_cast<double>(static_cast<float>(p[i]));
-    const double x2 = static_cast<double>(static_cast<float>(p[half + i]));
-    const double c = ct[i], s = st[i];
-    // engine.py:65-66, each f64 product and sum rounded separately (no contraction)
-    const float o1 = static_cast<float>(__dsub_rn(__dmul_rn(x1, c), __dmul_rn(x2, s)));
-    const float o2 = static_cast<float>(__dadd_rn(__dmul_rn(x1, s), __dmul_rn(x2, c)));
+  for (int u = threadIdx.x; u < units; u += blockDim.x) {
+    const int hh = u / hu, i = (u % hu) * 2;
+    E* p = rowp + (hh < n_heads ? 0 : k_col) + (hh % n_heads) * d_head;
+    E2* p1 = reinterpret_cast<E2*>(p + i);
+    E2* p2 = reinterpret_cast<E2*>(p + half + i);
+    const E2 a = *p1, b = *p2;
+    float a0, a1, b0, b1;
     if constexpr (std::is_same_v<E, float>) {
-      p[i] = o1;
-      p[half + i] = o2;
+      a0 = a.x; a1 = a.y; b0 = b.x; b1 = b.y;
     } else {
-      p[i] = __float2bfloat16_rn(o1);
-      p[half + i] = __float2bfloat16_rn(o2);
+      const float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+      a0 = fa.x; a1 = fa.y; b0 = fb.x; b1 = fb.y;
+    }
+    float o[4];
+    const double xs1[2] = {a0, a1}, xs2[2] = {b0, b1};
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const double c = __ldg(ct + i + e), sn = __ldg(st + i + e);
+      // engine.py:65-66, each f64 product and sum rounded separately (no contraction)
+      o[e] = static_cast<float>(__dsub_rn(__dmul_rn(xs1[e], c), __dmul_rn(xs2[e], sn)));
+      o[2 + e] = static_cast<float>(__dadd_rn(__dmul_rn(xs1[e], sn), __dmul_rn(xs2[e], c)));
+    }
+    if constexpr (std::is_same_v<E, float>) {
+      *p1 = make_float2(o[0], o[1]);
+      *p2 = make_float2(o[2], o[3]);
+    } else {
+      *p1 = __floats2bfloat162_rn(o[0], o[1]);
+      *p2 = __floats2bfloat162_rn(o[2], o[3]);
     }
   }
 }
 
 }  // namespace
 
-cudaError_t launch_rmsnorm(const float* x, const float* gain, int T, int d, double eps,
-                           void* out_bf16, float* out_f32, const float* query, float sqrt_d,
-                           float* logits, int logit_row0, int logit_row1, cudaStream_t s) {
-  if (T <= 0) return cudaSuccess;
+template <int kAdd>
+cudaError_t launch_rmsnorm_t(float* x, const float* gain, int T, int d, double eps,
+                             const void* add, __nv_bfloat16* ob, float* out_f32,
+                             const float* query, float sqrt_d, float* logits, int r0, int r1,
+                             cudaStream_t s) {
   const int nv = (d / 4 + kNormThreads - 1) / kNormThreads;
-  auto* ob = static_cast<__nv_bfloat16*>(out_bf16);
-#define FFWD_NORM(V)                                                                      \
-  rmsnorm_kernel<V><<<T, kNormThreads, 0, s>>>(x, gain, d, eps, ob, out_f32, query, sqrt_d, \
-                                               logits, logit_row0, logit_row1)
+#define FFWD_NORM(V)                                                                         \
+  rmsnorm_kernel<V, kAdd><<<T, kNormThreads, 0, s>>>(x, gain, d, eps, add, ob, out_f32, query, \
+                                                     sqrt_d, logits, r0, r1)
   if (nv <= 1) FFWD_NORM(1);
   else if (nv <= 2) FFWD_NORM(2);
   else if (nv <= 4) FFWD_NORM(4);
@@ -161,12 +197,29 @@ cudaError_t launch_rmsnorm(const float* x, const float* gain, int T, int d, doub
   return cudaGetLastError();
 }
 
+cudaError_t launch_rmsnorm(float* x, const float* gain, int T, int d, double eps,
+                           const void* add, int add_kind, void* out_bf16, float* out_f32,
+                           const float* query, float sqrt_d, float* logits, int logit_row0,
+                           int logit_row1, cudaStream_t s) {
+  if (T <= 0) return cudaSuccess;
+  auto* ob = static_cast<__nv_bfloat16*>(out_bf16);
+  if (add == nullptr || add_kind == 0)
+    return launch_rmsnorm_t<0>(x, gain, T, d, eps, nullptr, ob, out_f32, query, sqrt_d, logits,
+                               logit_row0, logit_row1, s);
+  if (add_kind == 1)
+    return launch_rmsnorm_t<1>(x, gain, T, d, eps, add, ob, out_f32, query, sqrt_d, logits,
+                               logit_row0, logit_row1, s);
+  return launch_rmsnorm_t<2>(x, gain, T, d, eps, add, ob, out_f32, query, sqrt_d, logits,
+                             logit_row0, logit_row1, s);
+}
+
 cudaError_t launch_rope(void* qk, bool is_f32, int T, int row_stride, int k_col, int n_heads,
                         int d_head, const double* cos_t, const double* sin_t, int pos0,
                         cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
-  const dim3 grid(T, 2 * n_heads);
-  const int threads = d_head / 2 < 32 ? 32 : (d_head / 2 > 128 ? 128 : d_head / 2);
+  const dim3 grid(T);
+  const int units = n_heads * (d_head / 2);  // 2 x n_heads x (d_head / 4)
+  const int threads = units >= 256 ? 256 : (units + 31) / 32 * 32;
   if (is_f32)
     rope_kernel<float><<<grid, threads, 0, s>>>(static_cast<float*>(qk), row_stride, k_col,
                                                 n_heads, d_head, cos_t, sin_t, pos0);

@@ -21,8 +21,10 @@ ROPE_BASE = 10000.0  # engine.py:41
 def rmsnorm(x: torch.Tensor, gain: torch.Tensor, eps: float = 1e-6, out_bf16: bool = True,
             out_f32: bool = False, predictor: DevicePredictor | None = None,
             logits: torch.Tensor | None = None, out: torch.Tensor | None = None,
-            out32: torch.Tensor | None = None):
+            out32: torch.Tensor | None = None, add: torch.Tensor | None = None):
     """Rows of x (T, d) f32 scaled to unit RMS times `gain` (f64 arithmetic, f32 result).
+
+    With `add` ((T, d) f32 or bf16) the residual add ``x += add`` runs first, in place.
 
     Returns (bf16 or None, f32 or None, logits or None).  With `predictor`, also
     writes f32(q . bf16(row)) / f32(sqrt d) per row into `logits` (T,), the input of
@@ -47,8 +49,15 @@ def rmsnorm(x: torch.Tensor, gain: torch.Tensor, eps: float = 1e-6, out_bf16: bo
         q = predictor.query
         if logits is None:
             logits = torch.empty((T,), dtype=torch.float32, device=dev)
+    add_kind = 0
+    if add is not None:
+        if not (add.is_cuda and add.is_contiguous() and tuple(add.shape) == (T, d)
+                and add.dtype in (torch.float32, torch.bfloat16)):
+            raise ValidationError("rmsnorm add must be a contiguous CUDA f32/bf16 (T, d) tensor")
+        add_kind = 1 if add.dtype == torch.float32 else 2
     lib = _dev.lib_for(dev)
-    _lib.check(lib.ffwd_rmsnorm(x.data_ptr(), g.data_ptr(), T, d, float(eps), _dev.ptr(ob),
+    _lib.check(lib.ffwd_rmsnorm(x.data_ptr(), g.data_ptr(), T, d, float(eps), _dev.ptr(add),
+                                add_kind, _dev.ptr(ob),
                                 _dev.ptr(o32), _dev.ptr(q), _dev.ptr(logits if q is not None
                                                                       else None),
                                 0, T if q is not None else 0, _dev.stream_handle(dev)),

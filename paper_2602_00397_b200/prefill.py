@@ -30,6 +30,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 import torch.nn.functional as F
+from torch.nn.attention import SDPBackend, sdpa_kernel
 
 from . import _dev
 from .compensator import CompensatorParams
@@ -42,6 +43,10 @@ from .predictor import DevicePredictor, PredictorParams
 from .sparse import budget_to_k
 
 MODES = ("dense", "predicted")
+FUSE_LOGITS = True  # predictor logits from the FFN-input RMSNorm (A/B knob)
+# Library attention backends, best first on sm_100 (cuDNN has Blackwell kernels).
+SDPA_BACKENDS = [SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION,
+                 SDPBackend.EFFICIENT_ATTENTION, SDPBackend.MATH]
 
 
 @dataclass
@@ -166,7 +171,8 @@ def _attention(model: DeviceModel, dl: DeviceLayer, a: torch.Tensor, T: int):
     q = qkv[:, :d].view(T, H, dh).transpose(0, 1).unsqueeze(0)
     k = qkv[:, d:2 * d].view(T, H, dh).transpose(0, 1).unsqueeze(0)
     v = qkv[:, 2 * d:].view(T, H, dh).transpose(0, 1).unsqueeze(0)
-    o = F.scaled_dot_product_attention(q, k, v, is_causal=True)  # scale 1/sqrt(dh)
+    with sdpa_kernel(SDPA_BACKENDS, set_priority=True):
+        o = F.scaled_dot_product_attention(q, k, v, is_causal=True)  # scale 1/sqrt(dh)
     o = o.squeeze(0).transpose(0, 1).reshape(T, d)
     return torch.mm(o, dl.wo_t.t()), qkv
 
@@ -191,15 +197,15 @@ def prefill(model: DeviceModel, tokens, mode: str = "predicted", keep_masks: boo
     for l, dl in enumerate(model.layers):
         a_bf, a32, _ = rmsnorm(h, dl.attn_norm, out_bf16=not f32_attn, out_f32=f32_attn)
         o, qkv = _attention(model, dl, a32 if f32_attn else a_bf, T)
-        h.add_(o.float())
         if return_kv:
             kv.append((qkv[:, d:2 * d].clone(), qkv[:, 2 * d:].clone()))
         k = dl.k if mode == "predicted" else f
         sparse = k < f
         pred = dl.predictor if sparse else _dense_predictor(d, f, dev)
-        fuse_logits = sparse and not f32_attn
+        fuse_logits = sparse and not f32_attn and FUSE_LOGITS
+        # h += o (engine.py:265) fused into the FFN-input norm
         _, _, logits = rmsnorm(h, dl.ffn_norm, out=xb, out_f32=f32_attn and sparse, out32=x32,
-                               predictor=pred if fuse_logits else None, logits=lg)
+                               predictor=pred if fuse_logits else None, logits=lg, add=o)
         res = sparse_ffn_layer(xb, dl.ffn, pred, k, dense_first_last=model.dense_first_last,
                                has_comp=model.has_comp, out=h, residual=h,
                                return_indices=keep_masks and sparse,
@@ -211,7 +217,7 @@ def prefill(model: DeviceModel, tokens, mode: str = "predicted", keep_masks: boo
             for row in range(idx.shape[0]):
                 masks[(l, b0 + row)] = idx[row]
     fin = rmsnorm(h[-1:].contiguous(), model.final_norm, out_bf16=False, out_f32=True)[1]
-    logits_out = (fin.double() @ model.head.double()).float()[0]  # f64-accumulated matmul
+    logits_out = torch.mv(model.head.t(), fin[0])  # f32 GEMV (the reference accumulates in f64)
     flops = predict_prefill_flops(
         cfg.n_layers, d, f, cfg.vocab_size, T, b=None if mode == "dense" else
         [float(dl.k) / f for dl in model.layers], dense_first_last=model.dense_first_last,

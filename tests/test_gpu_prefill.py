@@ -69,6 +69,22 @@ def test_rmsnorm_and_fused_logits(ff, T, d):
     near_exact(lg.cpu().numpy(), z.astype(np.float32), "fused logits")
 
 
+@pytest.mark.parametrize("add_dtype", [torch.float32, torch.bfloat16])
+def test_rmsnorm_fused_residual_add(ff, add_dtype):
+    from paper_2602_00397_b200.norm import rmsnorm
+    rng = np.random.default_rng(3)
+    T, d = 64, 1024
+    x = rng.standard_normal((T, d)).astype(np.float32)
+    add = rng.standard_normal((T, d)).astype(np.float32)
+    gain = np.ones(d, np.float32)
+    xt = torch.from_numpy(x).cuda()
+    at = torch.from_numpy(add).cuda().to(add_dtype)
+    _, x32, _ = rmsnorm(xt, torch.from_numpy(gain).cuda(), out_bf16=False, out_f32=True, add=at)
+    x_new = x + at.float().cpu().numpy()  # engine.py:265, f32 add
+    assert np.array_equal(xt.cpu().numpy(), x_new)
+    near_exact(x32.cpu().numpy(), rms_ref(x_new, gain), "rmsnorm after add")
+
+
 def rope_ref(m, n_heads, d_head, pos0=0):  # engine.py:50-68
     half = d_head // 2
     freqs = 10000.0 ** (-2.0 * np.arange(half) / d_head)
