@@ -338,11 +338,14 @@ def run_gpu(args, rank: int, world: int) -> None:
     if args.layers:
         L = args.layers
         CONFIGS[args.config] = (d, f, L, T, keep)
-    tp = world
-    layers, ks = make_layers(args.config, dev, rank, tp)
+    # tp: tensor parallel over d_ffn (one prompt, NCCL all-reduce per layer);
+    # dp: every rank runs the whole stack on its own prompt (independent prompts, no
+    # collective in the data path)
+    tp = world if args.parallel == "tp" else 1
+    layers, ks = make_layers(args.config, dev, rank if tp > 1 else 0, tp)
     n_blk = -(-T // 128)
     gx = torch.Generator(device=dev)
-    gx.manual_seed(99)
+    gx.manual_seed(99 + (rank if args.parallel == "dp" else 0))
     x0 = torch.randn((T, d), generator=gx, device=dev).to(torch.bfloat16).float()
     res = torch.empty_like(x0)
     xb = torch.empty((T, d), dtype=torch.bfloat16, device=dev)
@@ -416,7 +419,8 @@ def run_gpu(args, rank: int, world: int) -> None:
     flops_layer = [ff.ffn_path_flops(d, f, T, k) for k in ks]
     total_flops = sum(flops_layer)
     value = step_ms / L
-    eff_tflops = total_flops / (step_ms * 1e-3) / 1e12
+    prompts = world if args.parallel == "dp" else 1  # prompts processed per step, all ranks
+    eff_tflops = prompts * total_flops / (step_ms * 1e-3) / 1e12
     up_ms, up_n = stages["up_proj"]
     dn_ms, dn_n = stages["down_proj"]
     rc = ff.default_comp_dim(d)
@@ -435,12 +439,14 @@ def run_gpu(args, rank: int, world: int) -> None:
     out = {
         "metric": METRIC, "value": value, "unit": "ms/layer", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
-        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "higher_is_better": False, "scaling": "weak" if args.parallel == "dp" and world > 1
+        else "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init normal*0.02 weights, N(0,1) bf16 hidden states)",
         "config": {"workload": WORKLOAD_NAMES[args.config], "global_batch": 1, "seq_len": T,
                    "layers": L, "keep": keep, "k_per_layer": ks if args.config == "qwen8b"
                    else ks[0], "block": 128, "dense_first_last": True,
-                   "parallelism": f"tp{tp}" if tp > 1 else "single",
+                   "parallelism": f"tp{tp}" if tp > 1 else (f"dp{world}" if world > 1
+                                                            else "single"),
                    "l2": "inputs larger than L2 (X 128 MiB, 361 MiB weights per layer, "
                          "32 distinct layers per step); no flush"},
         "e2e": {"value": e2e_ms / L, "unit": "ms/layer", "h2d_bytes_per_step": h2d,
@@ -448,6 +454,7 @@ def run_gpu(args, rank: int, world: int) -> None:
                 "api": "paper_2602_00397_b200.sparse_ffn_layer (x from pinned host f32)"},
         "gpu_launches": launches,
         "effective_tflops": eff_tflops,
+        "prefill_ffn_tokens_per_s": prompts * T / (step_ms * 1e-3),
         "roofline": {"kernel": "up_proj (K2 gather-GEMM + SwiGLU)", "bound": "tensor",
                      "achieved": achieved, "peak": peaks["bf16_sus"], "unit": "TFLOP/s",
                      "frac": achieved / peaks["bf16_sus"],
@@ -509,6 +516,9 @@ def main():
     ap.add_argument("--skip-dense", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-ttft", action="store_true")
+    ap.add_argument("--parallel", default="tp", choices=["tp", "dp"],
+                    help="N>1: tensor parallel over d_ffn (one prompt) or data parallel "
+                         "(one prompt per GPU)")
     ap.add_argument("--raster", default="", help="UP,DOWN blocks per L2 raster group (tuning)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
