@@ -130,6 +130,44 @@ FFWD_API int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t,
                    size_t workspace_bytes, void* stream);
 
 /*
+ * Oracle scoring (sparse.py:94-115 oracle_experts / hidden_column_scores): the
+ * dense gate/up products of every 128-token block of x (identity index, no
+ * compensator), H = silu(x Wg) * (x Wu) in bf16, then per block and neuron
+ * scores[b][j] = f32(sqrt(sum_t H[t][j]^2)) (f64 sum).  tp_size 1 layout
+ * (f = d_ffn rows of gate^T / up^T in wgu_t).  scores: f32 [n_blk x f].
+ */
+FFWD_API size_t ffwd_hidden_scores_workspace_bytes(int T, int d, int f);
+FFWD_API int ffwd_hidden_scores(const void* x_bf16, int T, int d, const void* wgu_t, int f,
+                                int rc_local, float* scores, void* workspace,
+                                size_t workspace_bytes, void* stream);
+
+/*
+ * sparse.hidden_column_scores (sparse.py:94-97) of a hidden matrix h [n_rows x f]
+ * (row stride ld; f32 when is_f32 else bf16), per 128-row block:
+ * scores[b][j] = f32(sqrt(sum_t h[t][j]^2)), f64 sum.  scores: f32 [ceil(n/128) x f].
+ */
+FFWD_API int ffwd_column_norms(const void* h, int is_f32, int n_rows, int ld, int f,
+                               float* scores, void* stream);
+
+/*
+ * The FFN branch of engine.py:254-310 for the ablation modes (tp_size 1):
+ *   mode 1 "oracle": every sparse block is scored by its own dense gate/up pass
+ *                    (oracle_experts) and keeps its top-k;
+ *   mode 2 "static": block 0 runs dense and its hidden-norm top-k (mask_from_hidden,
+ *                    FirstBlockStatic) is used by every later sparse block.
+ * Dense blocks as in the engine (dense_first_last, static block 0, k >= f).
+ * idx_out (nullable) receives the masks: [n_scored x ld_idx_out] (1 row for static).
+ */
+FFWD_API size_t ffwd_ffn_layer_mode_workspace_bytes(int T, int d, int f, int rc_local, int k,
+                                                    int mode, int dense_first_last);
+FFWD_API int ffwd_ffn_layer_mode(const void* x_bf16, int T, int d, const void* wgu_t,
+                                 const void* wd, int f, int rc_local, int k, int mode,
+                                 int dense_first_last, int has_comp, float* y,
+                                 const float* residual, void* x_next_bf16, int32_t* idx_out,
+                                 int ld_idx_out, void* workspace, size_t workspace_bytes,
+                                 void* stream);
+
+/*
  * ffwd_ffn_layer with two optional predictor inputs (NULL = as ffwd_ffn_layer):
  *   x_pred_f32  f32 [T x d]: the predictor pools over these values instead of
  *               x_bf16 -- the reference predictor sees the f32 RMSNorm output

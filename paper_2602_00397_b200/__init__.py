@@ -12,13 +12,14 @@ from .predictor import (DevicePredictor, PredictorParams, default_reduced_dim, i
                         predictor_forward, predictor_scores)
 from .compensator import (CompensatorParams, apply_compensation, compensator_forward,
                           default_comp_dim, init_compensator)
-from .sparse import (ExpertMask, SubWeights, budget_to_k, build_mask, select_subweights,
+from .sparse import (ExpertMask, FirstBlockStatic, SubWeights, budget_to_k, build_mask,
+                     hidden_column_scores, mask_from_hidden, oracle_experts, select_subweights,
                      sparse_ffn_forward, topk_indices)
 from .scheduler import (AttentionMassProfile, SparsityPlan, allocate_budgets, budgets_to_topk,
                         dense_plan, load_plan, plan_from_profile, save_plan, uniform_plan)
 from .costmodel import FlopsReport, ffn_path_flops, predict_prefill_flops
-from .layer import (PackedLayer, dense_ffn, pack_layer, run_sparse_ffn, set_raster,
-                    shard_comp_cols, shard_neurons, sparse_ffn_layer)
+from .layer import (PackedLayer, dense_ffn, ffn_layer_mode, oracle_scores, pack_layer,
+                    run_sparse_ffn, set_raster, shard_comp_cols, shard_neurons, sparse_ffn_layer)
 
 __all__ = [name for name in dir() if not name.startswith("_")]
 __version__ = "0.1.0"

@@ -44,6 +44,14 @@ SIGNATURES = {
     "ffwd_ffn_layer2": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _vp, _vp, _vp,
                                  _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp,
                                  _vp, _vp, _vp, _c_int, _vp, _vp, _vp, _c_size, _vp]),
+    "ffwd_hidden_scores_workspace_bytes": (_c_size, [_c_int, _c_int, _c_int]),
+    "ffwd_hidden_scores": (_c_int, [_vp, _c_int, _c_int, _vp, _c_int, _c_int, _vp, _vp, _c_size,
+                                    _vp]),
+    "ffwd_column_norms": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _vp, _vp]),
+    "ffwd_ffn_layer_mode_workspace_bytes": (_c_size, [_c_int] * 7),
+    "ffwd_ffn_layer_mode": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int,
+                                     _c_int, _c_int, _c_int, _vp, _vp, _vp, _vp, _c_int, _vp,
+                                     _c_size, _vp]),
     "ffwd_rmsnorm": (_c_int, [_vp, _vp, _c_int, _c_int, ctypes.c_double, _vp, _c_int, _vp, _vp,
                               _vp, _vp, _c_int, _c_int, _vp]),
     "ffwd_rope": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp,

@@ -181,6 +181,11 @@ Ffn carve_ffn(Carve& c, int T, int d, int f_local, int rc_local, int kmax, int n
   return w;
 }
 
+Ffn carve_ffn_at(void* ws, int T, int d, int f_local, int rc_local, int k) {
+  Carve c(ws);
+  return carve_ffn(c, T, d, f_local, rc_local, k, 0, 4);
+}
+
 int check_common(int T, int d, int f, int k) {
   if (T < 1) return fail(FFWD_ERR_VALIDATION, "token count must be >= 1, got %d", T);
   if (d < 1 || f < 1) return fail(FFWD_ERR_VALIDATION, "bad dims d=%d f=%d", d, f);
@@ -191,7 +196,8 @@ int check_common(int T, int d, int f, int k) {
 int run_ffn(const void* x, int T, int d, const void* wgu_t, const void* wd, int f_local,
             int rc_local, const Ffn& w, const int32_t* idx, int ld_idx, int sparse_begin,
             int sparse_count, const int32_t* counts, int k_shared, int idx_shared, int has_comp,
-            float* y, const float* residual, void* x_next, cudaStream_t s) {
+            float* y, const float* residual, void* x_next, cudaStream_t s,
+            bool up_only = false) {
   const int n_blk = (T + kBlockTokens - 1) / kBlockTokens;
   PlanArgs pa{};
   pa.T = T;
@@ -242,6 +248,7 @@ int run_ffn(const void* x, int T, int d, const void* wgu_t, const void* wd, int 
     StageTimer tm(kUp, s);
     FFWD_CUDA(launch_up_proj(ga, s), "up_proj");
   }
+  if (up_only) return FFWD_OK;  // H only (oracle scoring)
   {
     StageTimer tm(kDown, s);
     FFWD_CUDA(launch_down_proj(ga, s), "down_proj");
@@ -455,6 +462,122 @@ int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t, const vo
                          k, dense_first_last, has_comp, tp_rank, tp_size, y, residual,
                          x_next_bf16, idx_global, ld_idx_global, nullptr, nullptr, workspace,
                          workspace_bytes, stream);
+}
+
+size_t ffwd_hidden_scores_workspace_bytes(int T, int d, int f) {
+  Carve c(nullptr);
+  carve_ffn(c, T, d, f, 0, f, 0, 4);
+  return c.off;
+}
+
+int ffwd_hidden_scores(const void* x_bf16, int T, int d, const void* wgu_t, int f,
+                       int rc_local, float* scores, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  g_err.clear();
+  int rc = check_common(T, d, f, f);
+  if (rc) return rc;
+  if ((rc = check_gemm_shapes(d, f))) return rc;
+  if (workspace_bytes < ffwd_hidden_scores_workspace_bytes(T, d, f))
+    return fail(FFWD_ERR_VALIDATION, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carve c(workspace);
+  Ffn w = carve_ffn(c, T, d, f, 0, f, 0, 4);
+  // dense gate/up over every block (identity index, no compensator): H = silu(g) * u
+  rc = run_ffn(x_bf16, T, d, wgu_t, nullptr, f, rc_local, w, nullptr, 0, 0, 0, nullptr, f, 0, 0,
+               nullptr, nullptr, nullptr, s, /*up_only=*/true);
+  if (rc) return rc;
+  FFWD_CUDA(launch_hidden_scores(w.h, false, w.hcols, T, f, scores, s), "hidden_scores");
+  return FFWD_OK;
+}
+
+int ffwd_column_norms(const void* h, int is_f32, int n_rows, int ld, int f, float* scores,
+                      void* stream) {
+  g_err.clear();
+  if (n_rows < 1 || f < 1 || ld < f)
+    return fail(FFWD_ERR_VALIDATION, "column_norms dims n=%d f=%d ld=%d", n_rows, f, ld);
+  FFWD_CUDA(launch_hidden_scores(h, is_f32 != 0, ld, n_rows, f, scores,
+                                 static_cast<cudaStream_t>(stream)),
+            "column_norms");
+  return FFWD_OK;
+}
+
+size_t ffwd_ffn_layer_mode_workspace_bytes(int T, int d, int f, int rc_local, int k, int mode,
+                                           int dense_first_last) {
+  const int n_blk = (T + kBlockTokens - 1) / kBlockTokens;
+  int b0 = 0, nb = 0;
+  layer_split(T, k, f, dense_first_last || mode == 2, &b0, &nb);
+  if (mode == 2 && !dense_first_last && k < f) nb = n_blk - 1;  // static: only block 0 dense
+  const int n_score = mode == 2 ? 1 : nb;
+  const int t_score = std::max(1, std::min(T - (mode == 2 ? 0 : b0) * kBlockTokens,
+                                           n_score * kBlockTokens));
+  Carve c(nullptr);
+  c.take<float>(static_cast<size_t>(std::max(1, n_score)) * f);           // scores
+  c.take<int32_t>(static_cast<size_t>(std::max(1, n_score)) * rup(k, 4));  // indices
+  const size_t a = c.off + ffwd_hidden_scores_workspace_bytes(t_score, d, f);
+  Carve c2(nullptr);
+  carve_ffn(c2, T, d, f, rc_local, k, 0, 4);
+  return std::max(a, c.off + c2.off);
+}
+
+int ffwd_ffn_layer_mode(const void* x_bf16, int T, int d, const void* wgu_t, const void* wd,
+                        int f, int rc_local, int k, int mode, int dense_first_last, int has_comp,
+                        float* y, const float* residual, void* x_next_bf16, int32_t* idx_out,
+                        int ld_idx_out, void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  int rc = check_common(T, d, f, k);
+  if (rc) return rc;
+  if ((rc = check_gemm_shapes(d, f))) return rc;
+  if (mode != 1 && mode != 2)
+    return fail(FFWD_ERR_VALIDATION, "mode %d: expected 1 (oracle) or 2 (static)", mode);
+  if (has_comp && rc_local < 1) return fail(FFWD_ERR_VALIDATION, "compensator width must be >= 1");
+  if (workspace_bytes <
+      ffwd_ffn_layer_mode_workspace_bytes(T, d, f, rc_local, k, mode, dense_first_last))
+    return fail(FFWD_ERR_VALIDATION, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n_blk = (T + kBlockTokens - 1) / kBlockTokens;
+  int b0 = 0, nb = 0;
+  // engine.py:256-262: dense if dense_first_last and j in {0, last}, or static and j == 0
+  layer_split(T, k, f, dense_first_last || mode == 2, &b0, &nb);
+  if (mode == 2 && !dense_first_last && k < f) nb = n_blk - 1;
+  if (idx_out && ld_idx_out < k) return fail(FFWD_ERR_VALIDATION, "ld_idx_out < k");
+  if (k >= f)  // full-K shortcut (engine.py:268): every block dense, no masks
+    return run_ffn(x_bf16, T, d, wgu_t, wd, f, rc_local, carve_ffn_at(workspace, T, d, f,
+                   rc_local, k), nullptr, 0, 0, 0, nullptr, f, 0, 0, y, residual, x_next_bf16, s);
+  // static scores block 0 even when no later block is sparse (the reference still
+  // records its mask, engine.py:273-277)
+  const int n_score = mode == 2 ? 1 : nb;
+  const int s_blk0 = mode == 2 ? 0 : b0;  // first scored block
+  Carve c(workspace);
+  float* scores = c.take<float>(static_cast<size_t>(std::max(1, n_score)) * f);
+  const int ld = rup(k, 4);
+  int32_t* idx = c.take<int32_t>(static_cast<size_t>(std::max(1, n_score)) * ld);
+  const size_t off = c.off;
+  if (n_score > 0) {
+    const int t_score = std::min(T - s_blk0 * kBlockTokens, n_score * kBlockTokens);
+    // 1. dense gate/up of the scored blocks -> column norms (sparse.py:94-115 oracle_experts
+    //    / mask_from_hidden); counted like the reference (costmodel oracle: 4 n d f)
+    rc = ffwd_hidden_scores(static_cast<const __nv_bfloat16*>(x_bf16) +
+                                static_cast<size_t>(s_blk0) * kBlockTokens * d,
+                            t_score, d, wgu_t, f, rc_local, scores,
+                            static_cast<char*>(workspace) + off, workspace_bytes - off, stream);
+    if (rc) return rc;
+    // 2. top-k of the scores (build_mask)
+    FFWD_CUDA(launch_topk(scores, n_score, f, k, 0, 1, nullptr, 0, idx, ld, nullptr, s), "topk");
+    if (idx_out)
+      FFWD_CUDA(cudaMemcpy2DAsync(idx_out, static_cast<size_t>(ld_idx_out) * 4, idx,
+                                  static_cast<size_t>(ld) * 4, static_cast<size_t>(k) * 4,
+                                  n_score, cudaMemcpyDeviceToDevice, s),
+                "idx copy");
+  }
+  if (nb == 0)  // no sparse block: the dense FFN over every block
+    return run_ffn(x_bf16, T, d, wgu_t, wd, f, rc_local,
+                   carve_ffn_at(static_cast<char*>(workspace) + off, T, d, f, rc_local, k),
+                   nullptr, 0, 0, 0, nullptr, f, 0, 0, y, residual, x_next_bf16, s);
+  // 3. sparse FFN (+ compensator) with those masks; static: one mask for every block
+  Carve c2(static_cast<char*>(workspace) + off);
+  Ffn w = carve_ffn(c2, T, d, f, rc_local, k, 0, 4);
+  return run_ffn(x_bf16, T, d, wgu_t, wd, f, rc_local, w, idx, ld, b0, nb, nullptr, k,
+                 mode == 2 ? 1 : 0, has_comp, y, residual, x_next_bf16, s);
 }
 
 int ffwd_rmsnorm(float* x, const float* gain, int T, int d, double eps, const void* add,

@@ -50,6 +50,9 @@ cudaError_t launch_rmsnorm(float* x, const float* gain, int T, int d, double eps
                            const void* add, int add_kind, void* out_bf16, float* out_f32,
                            const float* query, float sqrt_d, float* logits, int logit_row0,
                            int logit_row1, cudaStream_t s);
+// sparse.hidden_column_scores over bf16 H [n_blk*128 x hcols] -> scores [n_blk x f]
+cudaError_t launch_hidden_scores(const void* h, bool is_f32, int ld, int T, int f,
+                                 float* scores, cudaStream_t s);
 cudaError_t launch_rope(void* qk, bool is_f32, int T, int row_stride, int k_col, int n_heads,
                         int d_head, const double* cos_t, const double* sin_t, int pos0,
                         cudaStream_t s);

@@ -231,3 +231,48 @@ cudaError_t launch_rope(void* qk, bool is_f32, int T, int row_stride, int k_col,
 }
 
 }  // namespace ffwd
+
+// ------------------------------------------------------------ hidden column scores
+// sparse.hidden_column_scores (sparse.py:94-97): per block b and neuron j,
+// f32(sqrt(sum_t h[t][j]^2)) with f64 accumulation over the block's valid tokens.
+// H: the bf16 gated activation of the dense up-projection, or any f32 hidden matrix.
+namespace ffwd {
+namespace {
+
+template <typename E>
+__global__ void __launch_bounds__(256)
+    hidden_scores_kernel(const E* __restrict__ h, int ld, int T, int f,
+                         float* __restrict__ scores) {
+  const int b = blockIdx.y;
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  if (j >= f) return;
+  const int t0 = b * kBlockTokens, n = min(kBlockTokens, T - t0);
+  const E* col = h + static_cast<size_t>(t0) * ld + j;
+  double s = 0.0;
+#pragma unroll 8
+  for (int t = 0; t < n; ++t) {
+    double v;
+    if constexpr (std::is_same_v<E, float>) v = static_cast<double>(col[static_cast<size_t>(t) * ld]);
+    else v = static_cast<double>(__bfloat162float(col[static_cast<size_t>(t) * ld]));
+    s = fma(v, v, s);
+  }
+  scores[static_cast<size_t>(b) * f + j] = static_cast<float>(sqrt(s));
+}
+
+}  // namespace
+
+cudaError_t launch_hidden_scores(const void* h, bool is_f32, int ld, int T, int f,
+                                 float* scores, cudaStream_t s) {
+  const int n_blk = (T + kBlockTokens - 1) / kBlockTokens;
+  if (n_blk <= 0 || f <= 0) return cudaSuccess;
+  const dim3 grid((f + 255) / 256, n_blk);
+  if (is_f32)
+    hidden_scores_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(h), ld, T, f,
+                                                     scores);
+  else
+    hidden_scores_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(h), ld, T, f, scores);
+  return cudaGetLastError();
+}
+
+}  // namespace ffwd

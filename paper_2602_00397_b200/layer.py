@@ -236,6 +236,77 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
     return y
 
 
+MODES = ("predicted", "oracle", "static")
+_MODE_CODE = {"oracle": 1, "static": 2}
+
+
+def oracle_scores(x, packed: PackedLayer) -> torch.Tensor:
+    """Dense-scoring pass of ``oracle_experts`` over every 128-token block of x (T, d):
+    H = silu(x Wg) * (x Wu) on the up-projection kernel, then per-block column norms
+    (``hidden_column_scores``).  Returns f32 (n_blk, d_ffn).  tp_size 1 only."""
+    if packed.tp_size != 1:
+        raise ValidationError("oracle scoring needs the unsharded layer (tp_size 1)")
+    dev = packed.device
+    xb = _x_bf16(x, dev)
+    T, d = xb.shape
+    if d != packed.d:
+        raise ValidationError(f"x width {d} != d_model {packed.d}")
+    lib = _dev.lib_for(dev)
+    f = packed.f_local
+    n_blk = -(-T // BLOCK)
+    out = torch.empty((n_blk, f), dtype=torch.float32, device=dev)
+    ws = _dev.workspace(dev, lib.ffwd_hidden_scores_workspace_bytes(T, d, f))
+    _lib.check(lib.ffwd_hidden_scores(xb.data_ptr(), T, d, packed.wgu_t.data_ptr(), f,
+                                      packed.rc_local, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                      _dev.stream_handle(dev)), "hidden_scores")
+    return out
+
+
+def ffn_layer_mode(x, packed: PackedLayer, k: int, mode: str, dense_first_last: bool = True,
+                   has_comp: bool = True, out: torch.Tensor | None = None,
+                   residual: torch.Tensor | None = None, x_next: torch.Tensor | None = None,
+                   return_indices: bool = False):
+    """The FFN branch of ``engine.py:254-310`` in the ablation modes (tp_size 1).
+
+    ``oracle``: each sparse block keeps the top-k of its own dense hidden norms
+    (``oracle_experts``); ``static``: block 0 runs dense and its mask serves every later
+    block (``FirstBlockStatic``, ``engine.py:272-283``).  Dense blocks and the full-K
+    shortcut as in the engine.  Returns y (and the masks, int32 rows, with
+    ``return_indices``: one row per sparse block for oracle, one row for static).
+    """
+    if mode not in _MODE_CODE:
+        raise ValidationError(f"unknown mode {mode!r}; expected one of {tuple(_MODE_CODE)}")
+    if packed.tp_size != 1:
+        raise ValidationError("the ablation modes need the unsharded layer (tp_size 1)")
+    dev = packed.device
+    xb = _x_bf16(x, dev)
+    T, d = xb.shape
+    f = packed.f_local
+    if not 1 <= k <= f:
+        raise ValidationError(f"k={k} out of range [1, {f}]")
+    lib = _dev.lib_for(dev)
+    y = out if out is not None else torch.empty((T, d), dtype=torch.float32, device=dev)
+    n_blk = -(-T // BLOCK)
+    if mode == "static":
+        n_rows = 1 if k < f else 0
+    else:
+        n_rows = 0 if k >= f else (max(0, n_blk - 2) if dense_first_last else n_blk)
+    idx = torch.empty((max(n_rows, 1), k), dtype=torch.int32, device=dev) \
+        if return_indices else None
+    code = _MODE_CODE[mode]
+    hc = int(has_comp and packed.rc_local > 0)
+    ws = _dev.workspace(dev, lib.ffwd_ffn_layer_mode_workspace_bytes(
+        T, d, f, packed.rc_local, k, code, int(dense_first_last)))
+    _lib.check(lib.ffwd_ffn_layer_mode(
+        xb.data_ptr(), T, d, packed.wgu_t.data_ptr(), packed.wd.data_ptr(), f, packed.rc_local,
+        k, code, int(dense_first_last), hc, y.data_ptr(), _dev.ptr(residual), _dev.ptr(x_next),
+        _dev.ptr(idx), k if idx is not None else 0, ws.data_ptr(), ws.numel(),
+        _dev.stream_handle(dev)), "ffn_layer_mode")
+    if return_indices:
+        return y, idx[:n_rows]
+    return y
+
+
 def set_raster(up_group: int, down_group: int) -> None:
     """Blocks per L2 raster group of the up / down gather-GEMMs (tuning knob)."""
     _lib.check(_lib.load_library().ffwd_set_raster(up_group, down_group), "set_raster")

@@ -36,13 +36,13 @@ from . import _dev
 from .compensator import CompensatorParams
 from .costmodel import FlopsReport, predict_prefill_flops
 from .errors import ValidationError
-from .layer import BLOCK, PackedLayer, pack_layer, sparse_ffn_layer
+from .layer import BLOCK, PackedLayer, ffn_layer_mode, oracle_scores, pack_layer, sparse_ffn_layer
 from .model import ModelConfig
 from .norm import apply_rope, rmsnorm
 from .predictor import DevicePredictor, PredictorParams
-from .sparse import budget_to_k
+from .sparse import budget_to_k, topk_device
 
-MODES = ("dense", "predicted")
+MODES = ("dense", "oracle", "predicted", "static")
 FUSE_LOGITS = True  # predictor logits from the FFN-input RMSNorm (A/B knob)
 # Library attention backends, best first on sm_100 (cuDNN has Blackwell kernels).
 SDPA_BACKENDS = [SDPBackend.CUDNN_ATTENTION, SDPBackend.FLASH_ATTENTION,
@@ -132,6 +132,7 @@ class PrefillResult:
     flops: FlopsReport
     masks: dict | None = None       # (layer, block) -> int64 ascending neuron ids
     kv: list | None = None          # per layer (rotated K, V), each (T, d)
+    recall_per_layer: np.ndarray | None = None
     extra: dict = field(default_factory=dict)
 
 
@@ -178,8 +179,15 @@ def _attention(model: DeviceModel, dl: DeviceLayer, a: torch.Tensor, T: int):
 
 
 def prefill(model: DeviceModel, tokens, mode: str = "predicted", keep_masks: bool = False,
-            return_kv: bool = False) -> PrefillResult:
-    """Prefill `tokens` through every layer; returns the hidden states and last logits."""
+            return_kv: bool = False, compute_recall: bool = False) -> PrefillResult:
+    """Prefill `tokens` through every layer; returns the hidden states and last logits.
+
+    Modes as ``engine.py:170-180``: ``dense``; ``predicted`` (the hot path); ``oracle``
+    (each sparse block keeps the top-k of its own dense hidden norms); ``static`` (block
+    0 dense, its masks reused by every later block).  ``compute_recall`` (predicted
+    mode) measures each layer's mask recall against the oracle masks with an extra,
+    uncounted dense scoring pass (``engine.py:192-199, 301-305``).
+    """
     if mode not in MODES:
         raise ValidationError(f"unknown mode {mode!r}; expected one of {MODES}")
     cfg = model.config
@@ -194,28 +202,55 @@ def prefill(model: DeviceModel, tokens, mode: str = "predicted", keep_masks: boo
     xb = torch.empty((T, d), dtype=torch.bfloat16, device=dev)
     x32 = torch.empty((T, d), dtype=torch.float32, device=dev) if f32_attn else None
     lg = torch.empty((T,), dtype=torch.float32, device=dev)
+    recall = np.full(cfg.n_layers, np.nan) if (compute_recall and mode == "predicted") else None
     for l, dl in enumerate(model.layers):
         a_bf, a32, _ = rmsnorm(h, dl.attn_norm, out_bf16=not f32_attn, out_f32=f32_attn)
         o, qkv = _attention(model, dl, a32 if f32_attn else a_bf, T)
         if return_kv:
             kv.append((qkv[:, d:2 * d].clone(), qkv[:, 2 * d:].clone()))
-        k = dl.k if mode == "predicted" else f
+        k = f if mode == "dense" else dl.k
         sparse = k < f
+        if mode in ("oracle", "static") and sparse:
+            rmsnorm(h, dl.ffn_norm, out=xb, add=o)   # h += o (engine.py:265), x = norm(h)
+            res = ffn_layer_mode(xb, dl.ffn, k, mode, dense_first_last=model.dense_first_last,
+                                 has_comp=model.has_comp, out=h, residual=h,
+                                 return_indices=keep_masks)
+            if keep_masks:
+                idx = res[1].cpu().numpy().astype(np.int64)
+                if mode == "static":  # engine.py:273-277 and :306-307: one mask, every block
+                    last = n_blk - 1 if model.dense_first_last else n_blk
+                    for j in [0] + list(range(1, last)):
+                        masks[(l, j)] = idx[0]
+                else:
+                    b0 = 1 if model.dense_first_last else 0
+                    for row in range(idx.shape[0]):
+                        masks[(l, b0 + row)] = idx[row]
+            continue
         pred = dl.predictor if sparse else _dense_predictor(d, f, dev)
         fuse_logits = sparse and not f32_attn and FUSE_LOGITS
         # h += o (engine.py:265) fused into the FFN-input norm
         _, _, logits = rmsnorm(h, dl.ffn_norm, out=xb, out_f32=f32_attn and sparse, out32=x32,
                                predictor=pred if fuse_logits else None, logits=lg, add=o)
+        want_idx = (keep_masks or recall is not None) and sparse
+        if recall is not None and sparse:  # oracle masks of the same inputs (uncounted)
+            osc = oracle_scores(xb, dl.ffn)
         res = sparse_ffn_layer(xb, dl.ffn, pred, k, dense_first_last=model.dense_first_last,
                                has_comp=model.has_comp, out=h, residual=h,
-                               return_indices=keep_masks and sparse,
+                               return_indices=want_idx,
                                x_pred_f32=x32 if (f32_attn and sparse) else None,
                                logits_in=logits if fuse_logits else None)
-        if keep_masks and sparse:
-            idx = res[1].cpu().numpy().astype(np.int64)
+        if want_idx:
             b0 = 1 if model.dense_first_last else 0
-            for row in range(idx.shape[0]):
-                masks[(l, b0 + row)] = idx[row]
+            idx = res[1]
+            if recall is not None and idx.shape[0] > 0:
+                oidx = topk_device(osc[b0:b0 + idx.shape[0]], k)
+                inter = torch.stack([torch.isin(idx[r], oidx[r]).sum()
+                                     for r in range(idx.shape[0])])
+                recall[l] = float(inter.double().mean() / k)
+            if keep_masks:
+                idx = idx.cpu().numpy().astype(np.int64)
+                for row in range(idx.shape[0]):
+                    masks[(l, b0 + row)] = idx[row]
     fin = rmsnorm(h[-1:].contiguous(), model.final_norm, out_bf16=False, out_f32=True)[1]
     logits_out = torch.mv(model.head.t(), fin[0])  # f32 GEMV (the reference accumulates in f64)
     flops = predict_prefill_flops(
@@ -223,4 +258,4 @@ def prefill(model: DeviceModel, tokens, mode: str = "predicted", keep_masks: boo
         [float(dl.k) / f for dl in model.layers], dense_first_last=model.dense_first_last,
         mode=mode, has_compensators=model.has_comp)
     return PrefillResult(hidden=h, last_logits=logits_out, flops=flops, masks=masks, kv=kv,
-                         extra={"n_blocks": n_blk})
+                         recall_per_layer=recall, extra={"n_blocks": n_blk})

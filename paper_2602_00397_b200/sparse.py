@@ -140,3 +140,60 @@ def sparse_ffn_forward(x, sub: SubWeights):
     idx_t = torch.from_numpy(row).to(dev)
     y = run_sparse_ffn(x, packed, idx_t, k=k, has_comp=False, idx_per_block=False)
     return _dev.to_host_f32(y) if host else y
+
+
+def hidden_column_scores(hidden):
+    """Per-neuron L2 norm of gated activations across a block (``sparse.py:94-97``):
+    f32(sqrt(sum_t h^2)) with f64 accumulation, on the GPU (``ffwd_column_norms``)."""
+    host = _dev.is_host(hidden)
+    dev = _dev.device_of(hidden)
+    h = hidden if (not host and hidden.dtype in (torch.float32, torch.bfloat16)) else \
+        _dev.to_device(hidden, torch.float32, dev)
+    h = h.contiguous()
+    if h.dim() != 2:
+        raise ValidationError(f"hidden must be 2-D, got shape {tuple(h.shape)}")
+    n, f = h.shape
+    if n > 128:
+        raise ValidationError(f"one block of at most 128 tokens, got {n}")
+    out = torch.empty((1, f), dtype=torch.float32, device=dev)
+    lib = _dev.lib_for(dev)
+    _lib.check(lib.ffwd_column_norms(h.data_ptr(), int(h.dtype == torch.float32), n, f, f,
+                                     out.data_ptr(), _dev.stream_handle(dev)), "column_norms")
+    return out[0].cpu().numpy() if host else out[0]
+
+
+def mask_from_hidden(hidden, k: int, layer: int = -1, block: int = -1) -> ExpertMask:
+    """``sparse.py:100-102``: top-k of the hidden column norms."""
+    return build_mask(hidden_column_scores(hidden), k, layer=layer, block=block)
+
+
+def oracle_experts(x, lw: LayerWeights, k: int, layer: int = -1, block: int = -1) -> ExpertMask:
+    """Exact top-k mask from a dense scoring pass over the block (``sparse.py:105-115``).
+
+    The dense gate/up products run in the sm_100a up-projection (bf16 operands, f32
+    accumulation, bf16 H), so scores near the k-th boundary may order differently
+    from the reference's f32/f64 pass; this is an accuracy ceiling, not the hot path.
+    """
+    from .layer import oracle_scores, packed_for
+    dev = _dev.device_of(x)
+    packed = packed_for(lw, None, dev)
+    s = oracle_scores(x, packed)
+    if s.shape[0] != 1:
+        raise ValidationError(f"one block of at most 128 tokens, got {s.shape[0]} blocks")
+    return build_mask(s[0], k, layer=layer, block=block)
+
+
+class FirstBlockStatic:
+    """Reuse the first block's oracle masks for every later block (``sparse.py:118-137``)."""
+
+    def __init__(self):
+        self._masks: dict[int, ExpertMask] = {}
+
+    def set_first(self, layer: int, mask: ExpertMask) -> None:
+        self._masks[layer] = mask
+
+    def mask_for(self, layer: int) -> ExpertMask:
+        if layer not in self._masks:
+            raise ValidationError(f"static mask requested for layer {layer} before the first "
+                                  "block was processed")
+        return self._masks[layer]

@@ -199,8 +199,16 @@ def make_prefill_case(name="prefill_small", seed=2026, n_layers=2, d=256, f=768,
     tokens = np.random.default_rng([seed, 5]).integers(0, vocab, T)
     plan = uniform_plan(n_layers, budget)
     res = prefill_blockwise(w, tokens, plan, mode="predicted", predictors=preds,
-                            compensators=comps, keep_masks=True)
+                            compensators=comps, keep_masks=True, compute_recall=True)
     dense = prefill_dense(w, tokens)
+    extra = {}
+    for mode in ("oracle", "static"):
+        r = prefill_blockwise(w, tokens, plan, mode=mode, compensators=comps, keep_masks=True)
+        mk = sorted(r.masks)
+        extra[f"{mode}_mask_keys"] = np.array(mk, np.int32)
+        extra[f"{mode}_masks"] = np.stack([r.masks[kk].indices.astype(np.int32) for kk in mk])
+        extra[f"{mode}_hidden"] = r.hidden[::4].astype(np.float32)
+        extra[f"{mode}_flops_total"] = np.int64(r.flops.total())
     keys = sorted(res.masks)
     out = dict(seed=seed, n_layers=n_layers, d=d, f=f, n_heads=n_heads, vocab=vocab, T=T,
                budget=budget, k=budget_to_k(budget, f),
@@ -210,6 +218,7 @@ def make_prefill_case(name="prefill_small", seed=2026, n_layers=2, d=256, f=768,
                last_logits=res.last_logits, dense_hidden=dense.hidden[::4].astype(np.float32),
                dense_last_logits=dense.last_logits,
                flops_total=np.int64(res.flops.total()),
+               recall_per_layer=res.recall_per_layer, **extra,
                sha_model=sha(w.tok_emb, w.w_out, *[getattr(lw, n) for lw in w.layers for n in
                                                     ("wq", "wk", "wv", "wo", "w_gate", "w_up",
                                                      "w_down")]),

@@ -41,3 +41,26 @@ def test_model_weights_validation():
                        final_norm=m["final_norm"])
     with pytest.raises(ValidationError):
         bad.validate()
+
+
+def test_prefill_flop_report_ablation_modes():
+    from paper_2602_00397_b200 import predict_prefill_flops
+    c = load_prefill_case()
+    g = c["golden"]
+    L, d, f, V, T = (int(g[k]) for k in ("n_layers", "d", "f", "vocab", "T"))
+    for mode in ("oracle", "static"):
+        rep = predict_prefill_flops(L, d, f, V, T, b=[float(g["budget"])] * L,
+                                    dense_first_last=True, mode=mode, has_compensators=True)
+        assert rep.total() == int(g[f"{mode}_flops_total"]), mode
+
+
+def test_first_block_static_contract():
+    import pytest
+    from paper_2602_00397_b200 import ExpertMask, FirstBlockStatic
+    from paper_2602_00397_b200.errors import ValidationError
+    bank = FirstBlockStatic()
+    with pytest.raises(ValidationError):
+        bank.mask_for(0)
+    m = ExpertMask(bits=np.array([0, 1, 1, 0], np.uint8), k=2, layer=3, block=0)
+    bank.set_first(3, m)
+    assert bank.mask_for(3) is m
