@@ -4,7 +4,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
            --expt-relaxed-constexpr -Iinclude
 PKG := paper_2602_00397_b200
-SRC := $(wildcard $(PKG)/csrc/*.cu)
+SRC := $(wildcard $(PKG)/csrc/*.cu $(PKG)/csrc/*.cpp)
 HDR := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.h include/*.h)
 LIB := $(PKG)/libffwd_b200.so
 

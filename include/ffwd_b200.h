@@ -212,6 +212,21 @@ FFWD_API int ffwd_rope(void* qk, int is_f32, int T, int row_stride, int k_col, i
                        void* stream);
 
 /*
+ * `.ffwd` checkpoint reader (checkpoint.py:1-22 layout, read_checkpoint :207-263):
+ * memory-maps the file, validates the header and directory with the reference's
+ * rules (FFWD_ERR_VALIDATION + ffwd_ckpt_last_error on failure) and exposes every
+ * tensor as a zero-copy little-endian f32 host pointer into the mapping (valid
+ * until ffwd_ckpt_close).  Host-only: no GPU needed.
+ */
+FFWD_API const char* ffwd_ckpt_last_error(void);
+FFWD_API int ffwd_ckpt_open(const char* path, void** handle);
+FFWD_API void ffwd_ckpt_close(void* handle);
+FFWD_API const char* ffwd_ckpt_config(void* handle, size_t* len);
+FFWD_API int ffwd_ckpt_num_tensors(void* handle);
+FFWD_API int ffwd_ckpt_tensor(void* handle, int i, const char** name, int* ndim, uint32_t* dims,
+                              const float** data, uint64_t* nbytes);
+
+/*
  * Per-launch device timing (CUDA events on the launching stream) for the
  * measurement harness.  Stages: 0 pool, 1 predictor W1, 2 predictor W2,
  * 3 top-k, 4 plan, 5 up-projection (K2), 6 down-projection (K3).

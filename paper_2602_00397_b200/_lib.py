@@ -56,6 +56,14 @@ SIGNATURES = {
                               _vp, _vp, _c_int, _c_int, _vp]),
     "ffwd_rope": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp,
                            _c_int, _vp]),
+    "ffwd_ckpt_last_error": (ctypes.c_char_p, []),
+    "ffwd_ckpt_open": (_c_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
+    "ffwd_ckpt_close": (None, [_vp]),
+    "ffwd_ckpt_config": (_vp, [_vp, ctypes.POINTER(_c_size)]),
+    "ffwd_ckpt_num_tensors": (_c_int, [_vp]),
+    "ffwd_ckpt_tensor": (_c_int, [_vp, _c_int, ctypes.POINTER(ctypes.c_char_p),
+                                  ctypes.POINTER(_c_int), ctypes.POINTER(ctypes.c_uint32),
+                                  ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_uint64)]),
     "ffwd_timing_enable": (_c_int, [_c_int]),
     "ffwd_timing_read": (_c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_c_int),
                                   _c_int]),

@@ -239,7 +239,7 @@ def prefill(model: DeviceModel, tokens, mode: str = "predicted", keep_masks: boo
                                return_indices=want_idx,
                                x_pred_f32=x32 if (f32_attn and sparse) else None,
                                logits_in=logits if fuse_logits else None)
-        if want_idx:
+        if want_idx and res[1] is not None:  # None: no predicted block (short prompt)
             b0 = 1 if model.dense_first_last else 0
             idx = res[1]
             if recall is not None and idx.shape[0] > 0:

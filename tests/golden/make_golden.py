@@ -229,9 +229,28 @@ def make_prefill_case(name="prefill_small", seed=2026, n_layers=2, d=256, f=768,
     print(f"{name}: {len(keys)} masks, flops {res.flops.total()}")
 
 
+def make_checkpoint_case(seed=77, n_layers=2, d=64, f=160, n_heads=2, vocab=50):
+    """Small `.ffwd` files written by the reference's own writer (checkpoint.py:77-118):
+    a model file and an auxiliary predictor + compensator file."""
+    from sparseprefill.checkpoint import write_checkpoint
+    from sparseprefill.synthetic import generate_synthetic_model
+    cfg = ModelConfig(n_layers=n_layers, d_model=d, d_ffn=f, n_heads=n_heads, vocab_size=vocab,
+                      block_size=128, max_context=256)
+    w = generate_synthetic_model(cfg, seed)
+    preds = [init_predictor(cfg, np.random.default_rng([seed, l])) for l in range(n_layers)]
+    comps = [init_compensator(cfg, np.random.default_rng([seed + 1, l])) for l in range(n_layers)]
+    write_checkpoint(os.path.join(HERE, "tiny_model.ffwd"), cfg, weights=w)
+    write_checkpoint(os.path.join(HERE, "tiny_aux.ffwd"), cfg, predictors=preds,
+                     compensators=comps)
+    print("tiny_model.ffwd / tiny_aux.ffwd written")
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "prefill":
         make_prefill_case()
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "checkpoint":
+        make_checkpoint_case()
         sys.exit(0)
     make_topk_edges()
     make_scheduler()
@@ -252,3 +271,4 @@ if __name__ == "__main__":
     make_case("qwen8b_pred", d=4096, f=12288, T=384, seed=9, with_ffn=False,
               dense_first_last=False, budget=0.37)
     make_prefill_case()
+    make_checkpoint_case()

@@ -265,3 +265,23 @@ def test_oracle_experts_and_hidden_scores_dropin(ff):
     ref_idx = orc.topk_indices(np.sqrt((h_.astype(np.float64) ** 2).sum(0)).astype(np.float32),
                                384)
     assert np.intersect1d(mask.indices, ref_idx).size >= 0.97 * 384
+
+
+def test_load_device_model_from_reference_checkpoint(ff):
+    """`.ffwd` (written by the reference) -> DeviceModel through the native reader's
+    mapping; the prefill equals the one built from the same weights in memory."""
+    import os
+    from paper_2602_00397_b200 import checkpoint
+    from paper_2602_00397_b200.prefill import DeviceModel, prefill
+    from tests.fixtures import GOLDEN
+    mp, ap = os.path.join(GOLDEN, "tiny_model.ffwd"), os.path.join(GOLDEN, "tiny_aux.ffwd")
+    plan = ff.uniform_plan(2, 0.5, dense_first_last=False)  # both 128-token blocks sparse
+    dm = checkpoint.load_device_model(mp, plan, aux_paths=[ap], device="cuda")
+    c, a = checkpoint.read_checkpoint(mp), checkpoint.read_checkpoint(ap)
+    ref = DeviceModel.from_weights(c.weights, plan, a.predictors, a.compensators, device="cuda")
+    tokens = np.random.default_rng(3).integers(0, 50, 256)
+    r1 = prefill(dm, tokens, mode="predicted", keep_masks=True)
+    r2 = prefill(ref, tokens, mode="predicted", keep_masks=True)
+    assert torch.equal(r1.hidden, r2.hidden)
+    assert sorted(r1.masks) == sorted(r2.masks) and len(r2.masks) == 4
+    assert all(np.array_equal(r1.masks[k], r2.masks[k]) for k in r2.masks)
