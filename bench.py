@@ -8,9 +8,11 @@ Workload (N=1, BASELINE configs[2] at one GPU): Llama-3.1-8B FFN shape
 (r 256, r' 512), random-init weights (normal x 0.02, synthetic.py:33-43).
 
 One step = the prefill FFN stack: for each of the 32 layers (own weights, own
-predictor and compensator) the hot path -- predictor -> top-k -> sparse SwiGLU
-FFN + compensator -> residual add (engine.py:254-310 minus attention/RMSNorm) --
-over all 128 blocks.  `value` = device time per step / 32 (ms per layer),
+predictor and compensator) the FFN branch of engine.py:264-308 over all 128
+blocks -- the FFN-input RMSNorm of the f32 residual stream (fused with the
+predictor's per-token logits), predictor -> top-k -> sparse SwiGLU FFN +
+compensator -> residual add.  The norm keeps the stack numerically sane (an
+FFN-only stack without it overflows to inf by layer 6).  `value` = device time per step / 32 (ms per layer),
 inputs resident in HBM; `e2e` = the same stack through the public API with the
 prompt's hidden states copied from pinned host memory and the result copied
 back inside the timed region.  Every input (X 128 MiB, weights 361 MiB per
@@ -329,6 +331,7 @@ def measure_ttft(layers, cfg_name: str, dev, steps: int) -> dict:
 def run_gpu(args, rank: int, world: int) -> None:
     import paper_2602_00397_b200 as ff
     from paper_2602_00397_b200 import layer as fl
+    from paper_2602_00397_b200.norm import rmsnorm
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     if args.raster:
@@ -353,18 +356,22 @@ def run_gpu(args, rank: int, world: int) -> None:
     ws_bytes = max(fl.layer_workspace_bytes(T, p, dp.r, k, True) for p, dp, k in layers)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
 
+    gain = torch.ones(d, device=dev)            # ffn_norm gains (ones, synthetic.py:41)
+    lg = torch.empty((T,), dtype=torch.float32, device=dev)
+
     def stack(x_src: torch.Tensor):
+        # engine.py:267-308 per layer: x = rmsnorm(h, ffn_norm) (fused with the predictor's
+        # per-token logits), then predictor -> top-k -> sparse FFN + compensator, h += y
         res.copy_(x_src)
-        xb.copy_(x_src)
         for packed, dp, k in layers:
+            rmsnorm(res, gain, out=xb, predictor=dp, logits=lg)
             if tp == 1:
-                ff.sparse_ffn_layer(xb, packed, dp, k, out=res, residual=res, x_next=xb,
+                ff.sparse_ffn_layer(xb, packed, dp, k, out=res, residual=res, logits_in=lg,
                                     workspace=ws)
             else:
-                ff.sparse_ffn_layer(xb, packed, dp, k, out=ybuf, workspace=ws)
+                ff.sparse_ffn_layer(xb, packed, dp, k, out=ybuf, logits_in=lg, workspace=ws)
                 torch.distributed.all_reduce(ybuf)
                 res.add_(ybuf)
-                xb.copy_(res)
 
     def barrier():
         if world > 1:
@@ -397,6 +404,8 @@ def run_gpu(args, rank: int, world: int) -> None:
         step_ms = timed(lambda: stack(x0), args.steps)
     fl.timing_enable(False)
     stages = fl.timing_read()
+    if not bool(torch.isfinite(res).all()):
+        raise RuntimeError("non-finite residual stream after the FFN stack")
     clocks = clk.summary()
 
     # ---- e2e through the public API with host buffers
@@ -469,13 +478,19 @@ def run_gpu(args, rank: int, world: int) -> None:
     if world == 1 and not args.skip_dense:
         packed, dp, k = layers[0]
         xd = x0.to(torch.bfloat16)
-        ff.dense_ffn(xd, packed)  # warm-up: workspace allocation + first-launch setup
-        own_dense = timed(lambda: ff.dense_ffn(xd, packed), args.steps)
+
+        def own_dense_layer():  # same FFN-input norm as the sparse step, then the dense FFN
+            rmsnorm(x0, gain, out=xd)
+            return ff.dense_ffn(xd, packed)
+
+        own_dense_layer()  # warm-up: workspace allocation + first-launch setup
+        own_dense = timed(own_dense_layer, args.steps)
         # cuBLAS-class dense FFN: [Wg|Wu] fused GEMM, silu*mul, down GEMM (torch.matmul bf16)
         wgu = packed.wgu_t[:2 * packed.f_local]
         wdn = packed.wd[:packed.f_local]
 
         def cublas_ffn():
+            rmsnorm(x0, gain, out=xd)
             h = xd @ wgu.t()
             a = torch.nn.functional.silu(h[:, :packed.f_local]) * h[:, packed.f_local:]
             return a @ wdn

@@ -229,9 +229,9 @@ FFWD_API int ffwd_ckpt_tensor(void* handle, int i, const char** name, int* ndim,
 /*
  * Per-launch device timing (CUDA events on the launching stream) for the
  * measurement harness.  Stages: 0 pool, 1 predictor W1, 2 predictor W2,
- * 3 top-k, 4 plan, 5 up-projection (K2), 6 down-projection (K3).
- * ffwd_timing_read waits for the recorded events, writes per-stage summed
- * milliseconds and launch counts, and clears the record.
+ * 3 top-k, 4 plan, 5 up-projection (K2), 6 down-projection (K3), 7 FFN-input
+ * RMSNorm.  ffwd_timing_read waits for the recorded events, writes per-stage
+ * summed milliseconds and kernel-launch counts, and clears the record.
  */
 #define FFWD_N_STAGES 7
 FFWD_API int ffwd_timing_enable(int on);

@@ -45,12 +45,13 @@ int cuda_fail(cudaError_t e, const char* where) {
 int rup(int v, int m) { return (v + m - 1) / m * m; }
 
 // ---- optional per-launch event timing (measurement harness only)
-enum Stage { kPool = 0, kW1, kW2, kTopk, kPlan, kUp, kDown, kNumStages };
+enum Stage { kPool = 0, kW1, kW2, kTopk, kPlan, kUp, kDown, kNorm, kNumStages };
 const char* kStageNames[kNumStages] = {"pool", "predictor_w1", "predictor_w2", "topk",
-                                       "plan", "up_proj", "down_proj"};
+                                       "plan", "up_proj", "down_proj", "ffn_norm"};
 bool g_timing = false;
 struct Rec {
   int stage;
+  int kernels;  // kernel launches inside the timed stage
   cudaEvent_t a, b;
 };
 std::vector<Rec> g_recs;
@@ -68,11 +69,12 @@ cudaEvent_t take_event() {
 }
 
 struct StageTimer {
-  Rec r{-1, nullptr, nullptr};
+  Rec r{-1, 1, nullptr, nullptr};
   cudaStream_t s;
-  StageTimer(int stage, cudaStream_t st) : s(st) {
+  StageTimer(int stage, cudaStream_t st, int kernels = 1) : s(st) {
     if (!g_timing) return;
     r.stage = stage;
+    r.kernels = kernels;
     r.a = take_event();
     r.b = take_event();
     cudaEventRecord(r.a, s);
@@ -132,16 +134,16 @@ int run_predictor(const void* x, bool x_is_f32, int T, int d, int b0, int nb, co
                   cudaStream_t s, const float* logits_in = nullptr) {
   const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));  // predictor.py:76
   {
-    StageTimer tm(kPool, s);
+    StageTimer tm(kPool, s, logits_in ? 1 : 2);
     FFWD_CUDA(launch_pool(x, x_is_f32, T, d, b0, nb, query, sqrt_d, p.logits, p.pooled, logits_in, s),
               "pool");
   }
   {
-    StageTimer tm(kW1, s);
+    StageTimer tm(kW1, s, gemm_f64acc_partial_bytes(nb, d, r) > 0 ? 2 : 1);
     FFWD_CUDA(launch_gemm_f64acc(p.pooled, w1, p.hidden, nb, d, r, true, p.partial, s), "w1");
   }
   {
-    StageTimer tm(kW2, s);
+    StageTimer tm(kW2, s, gemm_f64acc_partial_bytes(nb, r, f) > 0 ? 2 : 1);
     FFWD_CUDA(launch_gemm_f64acc(p.hidden, w2, scores, nb, r, f, false, p.partial, s), "w2");
   }
   return FFWD_OK;
@@ -595,6 +597,7 @@ int ffwd_rmsnorm(float* x, const float* gain, int T, int d, double eps, const vo
     return fail(FFWD_ERR_VALIDATION, "rmsnorm logit rows [%d, %d) outside [0, %d)", logit_row0,
                 logit_row1, T);
   const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));  // predictor.py:76
+  StageTimer tm(kNorm, static_cast<cudaStream_t>(stream));
   FFWD_CUDA(launch_rmsnorm(x, gain, T, d, eps, add, add ? add_kind : 0, out_bf16, out_f32, query,
                            sqrt_d, logits, logit_row0, logit_row1,
                            static_cast<cudaStream_t>(stream)),
@@ -637,7 +640,7 @@ int ffwd_timing_read(double* ms_out, int* count_out, int n_stages) {
     if (e != cudaSuccess && rc == FFWD_OK) rc = cuda_fail(e, "timing_read");
     if (r.stage < n_stages) {
       if (ms_out) ms_out[r.stage] += ms;
-      if (count_out) count_out[r.stage] += 1;
+      if (count_out) count_out[r.stage] += r.kernels;
     }
     g_event_pool.push_back(r.a);
     g_event_pool.push_back(r.b);

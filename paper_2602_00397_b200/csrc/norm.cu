@@ -48,85 +48,112 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return s;
 }
 
-// One CTA per row; thread i owns the float4 groups {i + 256 j}, held in registers
-// between the two passes.  kMaxV = float4 groups per thread (d <= 1024 * kMaxV).
-// kAdd: 0 none, 1 f32, 2 bf16 -- the residual add x += add (engine.py:265) fused in
-// front of the norm; the updated x is written back.
+// Persistent CTAs (2 per SM) walk rows r = blockIdx.x + k gridDim.x; thread i owns the
+// float4 groups {i + 256 j} of a row.  The f32 -> f64 widening (F2F, 16 per clock per
+// SM) bounds this kernel, so the gain and the predictor query are widened once per CTA
+// into registers, each x element once (reused for the square and the output), and the
+// next row's loads are issued before the current row's reductions.
 template <int kMaxV, int kAdd>
-__global__ void __launch_bounds__(kNormThreads)
-    rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ gain, int d, double eps,
-                   const void* __restrict__ add, __nv_bfloat16* __restrict__ out_bf16,
+__global__ void __launch_bounds__(kNormThreads, 2)
+    rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ gain, int T, int d,
+                   double eps, const void* __restrict__ add, __nv_bfloat16* __restrict__ out_bf16,
                    float* __restrict__ out_f32, const float* __restrict__ query, float sqrt_d,
                    float* __restrict__ logits, int logit_row0, int logit_row1) {
   __shared__ double red[kNormThreads / 32];
-  const int row = blockIdx.x;
   const int nv = d / 4;
-  float4* xr = reinterpret_cast<float4*>(x + static_cast<size_t>(row) * d);
-  float4 v[kMaxV];
-  double ss = 0.0;
+  double gd[kMaxV][4], qd[kMaxV][4];
 #pragma unroll
   for (int j = 0; j < kMaxV; ++j) {
     const int g = threadIdx.x + kNormThreads * j;
-    v[j] = g < nv ? xr[g] : make_float4(0.f, 0.f, 0.f, 0.f);
-    if (kAdd != 0 && g < nv) {
-      float4 a4;
-      if constexpr (kAdd == 1) {
-        a4 = __ldg(reinterpret_cast<const float4*>(add) + static_cast<size_t>(row) * nv + g);
-      } else {
-        const uint2 raw =
-            __ldg(reinterpret_cast<const uint2*>(add) + static_cast<size_t>(row) * nv + g);
-        const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
-        const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
-        a4 = make_float4(lo.x, lo.y, hi.x, hi.y);
+    const float4 w = g < nv ? __ldg(reinterpret_cast<const float4*>(gain) + g)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 q = (query && g < nv) ? __ldg(reinterpret_cast<const float4*>(query) + g)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    gd[j][0] = w.x; gd[j][1] = w.y; gd[j][2] = w.z; gd[j][3] = w.w;
+    qd[j][0] = q.x; qd[j][1] = q.y; qd[j][2] = q.z; qd[j][3] = q.w;
+  }
+  auto load_row = [&](int row, float4 (&v)[kMaxV]) {
+    const float4* xr = reinterpret_cast<const float4*>(x + static_cast<size_t>(row) * d);
+#pragma unroll
+    for (int j = 0; j < kMaxV; ++j) {
+      const int g = threadIdx.x + kNormThreads * j;
+      v[j] = g < nv ? xr[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  float4 nxt[kMaxV];
+  int row = blockIdx.x;
+  if (row < T) load_row(row, nxt);
+  for (; row < T; row += gridDim.x) {
+    float4 v[kMaxV];
+#pragma unroll
+    for (int j = 0; j < kMaxV; ++j) v[j] = nxt[j];
+    if (kAdd != 0) {
+      float4* xr = reinterpret_cast<float4*>(x + static_cast<size_t>(row) * d);
+#pragma unroll
+      for (int j = 0; j < kMaxV; ++j) {
+        const int g = threadIdx.x + kNormThreads * j;
+        if (g >= nv) continue;
+        float4 a4;
+        if constexpr (kAdd == 1) {
+          a4 = __ldg(reinterpret_cast<const float4*>(add) + static_cast<size_t>(row) * nv + g);
+        } else {
+          const uint2 raw =
+              __ldg(reinterpret_cast<const uint2*>(add) + static_cast<size_t>(row) * nv + g);
+          const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+          const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+          a4 = make_float4(lo.x, lo.y, hi.x, hi.y);
+        }
+        v[j].x = __fadd_rn(v[j].x, a4.x);  // engine.py:265, f32 residual add
+        v[j].y = __fadd_rn(v[j].y, a4.y);
+        v[j].z = __fadd_rn(v[j].z, a4.z);
+        v[j].w = __fadd_rn(v[j].w, a4.w);
+        xr[g] = v[j];
       }
-      v[j].x = __fadd_rn(v[j].x, a4.x);
-      v[j].y = __fadd_rn(v[j].y, a4.y);
-      v[j].z = __fadd_rn(v[j].z, a4.z);
-      v[j].w = __fadd_rn(v[j].w, a4.w);
-      xr[g] = v[j];
     }
-    const double a = v[j].x, b = v[j].y, c = v[j].z, e = v[j].w;
-    ss += (a * a + b * b) + (c * c + e * e);
-  }
-  const double mean = block_sum(ss, red) / static_cast<double>(d);
-  const double scale = 1.0 / sqrt(mean + eps);  // kernels.py:105
-  const bool want_logit = query != nullptr && row >= logit_row0 && row < logit_row1;
-  double z = 0.0;
-  const float4* gr = reinterpret_cast<const float4*>(gain);
-  const float4* qr = reinterpret_cast<const float4*>(query);
+    if (row + static_cast<int>(gridDim.x) < T) load_row(row + gridDim.x, nxt);  // prefetch
+    double xd[kMaxV][4];
+    double ss = 0.0;
 #pragma unroll
-  for (int j = 0; j < kMaxV; ++j) {
-    const int g = threadIdx.x + kNormThreads * j;
-    if (g >= nv) continue;
-    const float4 w = __ldg(gr + g);
-    float4 o;
-    o.x = static_cast<float>(__dmul_rn(__dmul_rn(v[j].x, scale), w.x));
-    o.y = static_cast<float>(__dmul_rn(__dmul_rn(v[j].y, scale), w.y));
-    o.z = static_cast<float>(__dmul_rn(__dmul_rn(v[j].z, scale), w.z));
-    o.w = static_cast<float>(__dmul_rn(__dmul_rn(v[j].w, scale), w.w));
-    const size_t off = static_cast<size_t>(row) * d + 4 * static_cast<size_t>(g);
-    if (out_f32) reinterpret_cast<float4*>(out_f32 + off)[0] = o;
-    const __nv_bfloat162 lo = __floats2bfloat162_rn(o.x, o.y);
-    const __nv_bfloat162 hi = __floats2bfloat162_rn(o.z, o.w);
-    if (out_bf16) {
-      uint2 pk;
-      pk.x = *reinterpret_cast<const uint32_t*>(&lo);
-      pk.y = *reinterpret_cast<const uint32_t*>(&hi);
-      reinterpret_cast<uint2*>(out_bf16 + off)[0] = pk;
+    for (int j = 0; j < kMaxV; ++j) {
+      xd[j][0] = v[j].x; xd[j][1] = v[j].y; xd[j][2] = v[j].z; xd[j][3] = v[j].w;
+      ss += (xd[j][0] * xd[j][0] + xd[j][1] * xd[j][1]) +
+            (xd[j][2] * xd[j][2] + xd[j][3] * xd[j][3]);
     }
-    if (want_logit) {  // q . bf16(x), the operand the pooling pass would read
-      const float4 q = __ldg(qr + g);
-      const float2 l2 = __bfloat1622float2(lo), h2 = __bfloat1622float2(hi);
-      z = fma(static_cast<double>(q.x), static_cast<double>(l2.x), z);
-      z = fma(static_cast<double>(q.y), static_cast<double>(l2.y), z);
-      z = fma(static_cast<double>(q.z), static_cast<double>(h2.x), z);
-      z = fma(static_cast<double>(q.w), static_cast<double>(h2.y), z);
+    const double mean = block_sum(ss, red) / static_cast<double>(d);
+    const double scale = 1.0 / sqrt(mean + eps);  // kernels.py:105
+    const bool want_logit = query != nullptr && row >= logit_row0 && row < logit_row1;
+    double z = 0.0;
+#pragma unroll
+    for (int j = 0; j < kMaxV; ++j) {
+      const int g = threadIdx.x + kNormThreads * j;
+      if (g >= nv) continue;
+      float o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        o[e] = static_cast<float>(__dmul_rn(__dmul_rn(xd[j][e], scale), gd[j][e]));
+      const size_t off = static_cast<size_t>(row) * d + 4 * static_cast<size_t>(g);
+      if (out_f32) reinterpret_cast<float4*>(out_f32 + off)[0] = make_float4(o[0], o[1], o[2], o[3]);
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(o[0], o[1]);
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(o[2], o[3]);
+      if (out_bf16) {
+        uint2 pk;
+        pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+        reinterpret_cast<uint2*>(out_bf16 + off)[0] = pk;
+      }
+      if (want_logit) {  // q . bf16(x), the operand the pooling pass would read
+        const float2 l2 = __bfloat1622float2(lo), h2 = __bfloat1622float2(hi);
+        z = fma(qd[j][0], static_cast<double>(l2.x), z);
+        z = fma(qd[j][1], static_cast<double>(l2.y), z);
+        z = fma(qd[j][2], static_cast<double>(h2.x), z);
+        z = fma(qd[j][3], static_cast<double>(h2.y), z);
+      }
     }
-  }
-  if (query != nullptr && row >= logit_row0 && row < logit_row1) {
-    const double zs = block_sum(z, red);
-    if (threadIdx.x == 0)
-      logits[row - logit_row0] = __fdiv_rn(static_cast<float>(zs), sqrt_d);  // predictor.py:76
+    if (want_logit) {
+      const double zs = block_sum(z, red);
+      if (threadIdx.x == 0)
+        logits[row - logit_row0] = __fdiv_rn(static_cast<float>(zs), sqrt_d);  // predictor.py:76
+    }
   }
 }
 
@@ -184,9 +211,13 @@ cudaError_t launch_rmsnorm_t(float* x, const float* gain, int T, int d, double e
                              const float* query, float sqrt_d, float* logits, int r0, int r1,
                              cudaStream_t s) {
   const int nv = (d / 4 + kNormThreads - 1) / kNormThreads;
-#define FFWD_NORM(V)                                                                         \
-  rmsnorm_kernel<V, kAdd><<<T, kNormThreads, 0, s>>>(x, gain, d, eps, add, ob, out_f32, query, \
-                                                     sqrt_d, logits, r0, r1)
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = T < 2 * sms ? T : 2 * sms;
+#define FFWD_NORM(V)                                                                       \
+  rmsnorm_kernel<V, kAdd><<<grid, kNormThreads, 0, s>>>(x, gain, T, d, eps, add, ob, out_f32, \
+                                                        query, sqrt_d, logits, r0, r1)
   if (nv <= 1) FFWD_NORM(1);
   else if (nv <= 2) FFWD_NORM(2);
   else if (nv <= 4) FFWD_NORM(4);

@@ -312,7 +312,8 @@ def set_raster(up_group: int, down_group: int) -> None:
     _lib.check(_lib.load_library().ffwd_set_raster(up_group, down_group), "set_raster")
 
 
-STAGES = ("pool", "predictor_w1", "predictor_w2", "topk", "plan", "up_proj", "down_proj")
+STAGES = ("pool", "predictor_w1", "predictor_w2", "topk", "plan", "up_proj", "down_proj",
+          "ffn_norm")
 
 
 def timing_enable(on: bool = True) -> None:
