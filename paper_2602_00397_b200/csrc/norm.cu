@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kNormThreads, 2)
     const double mean = block_sum(ss, red) / static_cast<double>(d);
     const double scale = 1.0 / sqrt(mean + eps);  // kernels.py:105
     const bool want_logit = query != nullptr && row >= logit_row0 && row < logit_row1;
-    double z = 0.0;
+    double z[4] = {0.0, 0.0, 0.0, 0.0};  // four independent DFMA chains
 #pragma unroll
     for (int j = 0; j < kMaxV; ++j) {
       const int g = threadIdx.x + kNormThreads * j;
@@ -143,14 +143,14 @@ __global__ void __launch_bounds__(kNormThreads, 2)
       }
       if (want_logit) {  // q . bf16(x), the operand the pooling pass would read
         const float2 l2 = __bfloat1622float2(lo), h2 = __bfloat1622float2(hi);
-        z = fma(qd[j][0], static_cast<double>(l2.x), z);
-        z = fma(qd[j][1], static_cast<double>(l2.y), z);
-        z = fma(qd[j][2], static_cast<double>(h2.x), z);
-        z = fma(qd[j][3], static_cast<double>(h2.y), z);
+        z[0] = fma(qd[j][0], static_cast<double>(l2.x), z[0]);
+        z[1] = fma(qd[j][1], static_cast<double>(l2.y), z[1]);
+        z[2] = fma(qd[j][2], static_cast<double>(h2.x), z[2]);
+        z[3] = fma(qd[j][3], static_cast<double>(h2.y), z[3]);
       }
     }
     if (want_logit) {
-      const double zs = block_sum(z, red);
+      const double zs = block_sum((z[0] + z[1]) + (z[2] + z[3]), red);
       if (threadIdx.x == 0)
         logits[row - logit_row0] = __fdiv_rn(static_cast<float>(zs), sqrt_d);  // predictor.py:76
     }
