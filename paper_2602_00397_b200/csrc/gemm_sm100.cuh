@@ -32,13 +32,26 @@ namespace {
 constexpr int BM = 128;           // tokens per tile (one block)
 constexpr int BK = 64;             // K per stage: 64 bf16 = one 128 B swizzle row
 constexpr int kStages = 4;
+// Split rings (FFWD_SPLIT_RING): the gathered B operand gets a deeper ring than the
+// 2-D A tile, which a dedicated warp loads on its own barriers.  The gathers' fill
+// latency is what the ring has to cover, and a shallower A ring frees the smem.
+#ifdef FFWD_SPLIT_RING
+constexpr bool kSplit = true;
+constexpr int kStagesA = FFWD_STAGES_A;
+constexpr int kStagesB = FFWD_STAGES_B;
+#else
+constexpr bool kSplit = false;
+constexpr int kStagesA = kStages;
+constexpr int kStagesB = kStages;
+#endif
 #ifndef FFWD_PRODUCER_WARPS
 #define FFWD_PRODUCER_WARPS 8
 #endif
 constexpr int kProducerWarps = FFWD_PRODUCER_WARPS;  // TMA gather4 issue rate scales with warps
 constexpr int kEpiWarp0 = kProducerWarps;            // multiple of 4: warp % 4 = TMEM lane quadrant
 constexpr int kMmaWarp = kProducerWarps + 4;
-constexpr int kThreads = (kProducerWarps + 5) * 32;
+constexpr int kAWarp = kProducerWarps + 5;  // A loader (split rings only)
+constexpr int kThreads = (kProducerWarps + 5 + (kSplit ? 1 : 0)) * 32;
 static_assert(kProducerWarps % 4 == 0 && 64 % kProducerWarps == 0, "producer split");
 constexpr uint32_t kTmemCols = 512;
 constexpr int kABytes = BM * BK * 2;  // 16 KiB
@@ -46,8 +59,10 @@ constexpr int kABytes = BM * BK * 2;  // 16 KiB
 __host__ __device__ constexpr int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 struct Barriers {
-  uint64_t full[kStages];
-  uint64_t empty[kStages];
+  uint64_t full[kStagesB];   // B (and, unsplit, A) landed
+  uint64_t empty[kStagesB];
+  uint64_t fullA[kStagesA];  // split rings: A landed / A slot free
+  uint64_t emptyA[kStagesA];
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint32_t tmem_base;
@@ -57,7 +72,8 @@ struct Barriers {
 
 template <int kBBytes>
 constexpr size_t smem_bytes() {
-  return 1024 + static_cast<size_t>(kStages) * (kABytes + kBBytes) + sizeof(Barriers);
+  return 1024 + static_cast<size_t>(kStagesA) * kABytes + static_cast<size_t>(kStagesB) * kBBytes +
+         sizeof(Barriers);
 }
 
 template <int kBBytes>
@@ -69,8 +85,8 @@ struct Smem {
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) &
                                                ~uintptr_t(1023));
     a = base;
-    b = base + kStages * kABytes;
-    bar = reinterpret_cast<Barriers*>(b + kStages * kBBytes);
+    b = base + kStagesA * kABytes;
+    bar = reinterpret_cast<Barriers*>(b + kStagesB * kBBytes);
   }
   __device__ uint8_t* a_stage(int s) const { return a + s * kABytes; }
   __device__ uint8_t* b_stage(int s) const { return b + s * kBBytes; }
@@ -79,9 +95,13 @@ struct Smem {
 template <int kBBytes>
 __device__ __forceinline__ void prologue(Smem<kBBytes>& sm, int warp) {
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < kStagesB; ++i) {
       mbar_init(&sm.bar->full[i], kProducerWarps);
       mbar_init(&sm.bar->empty[i], 1);
+    }
+    for (int i = 0; i < kStagesA; ++i) {
+      mbar_init(&sm.bar->fullA[i], 1);
+      mbar_init(&sm.bar->emptyA[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.bar->tfull[i], 1);
@@ -128,17 +148,48 @@ __device__ __forceinline__ void mma_tile(Smem<kBBytes>& sm, uint32_t tmem_d, int
                 (kb | kk) != 0 ? 1u : 0u);
     }
     umma_commit(&sm.bar->empty[stage]);
-    if (++stage == kStages) {
+    if (++stage == kStagesB) {
       stage = 0;
       phase ^= 1;
     }
   }
 }
 
-__device__ __forceinline__ void advance(uint32_t& stage, uint32_t& phase) {
-  if (++stage == kStages) {
+template <int N>
+__device__ __forceinline__ void advance_n(uint32_t& stage, uint32_t& phase) {
+  if (++stage == N) {
     stage = 0;
     phase ^= 1;
+  }
+}
+
+__device__ __forceinline__ void advance(uint32_t& stage, uint32_t& phase) {
+  advance_n<kStagesB>(stage, phase);
+}
+
+// Split rings: the MMA waits for the stage's A slot and B slot separately and
+// releases both.
+template <int kBBytes>
+__device__ __forceinline__ void mma_tile_split(Smem<kBBytes>& sm, uint32_t tmem_d, int nk,
+                                               uint32_t idesc, uint32_t b_lbo, uint32_t b_sbo,
+                                               uint32_t b_kstep, uint32_t& sb, uint32_t& pb,
+                                               uint32_t& sa, uint32_t& pa) {
+  for (int kb = 0; kb < nk; ++kb) {
+    mbar_wait(&sm.bar->fullA[sa], pa);
+    mbar_wait(&sm.bar->full[sb], pb);
+    tc_fence_after();
+    const uint64_t adesc = make_sdesc_sw128(smem_u32(sm.a_stage(sa)), 16, 1024);
+    const uint64_t bdesc = make_sdesc_sw128(smem_u32(sm.b_stage(sb)), b_lbo, b_sbo);
+#pragma unroll
+    for (int kk = 0; kk < BK / 16; ++kk) {
+      umma_bf16(tmem_d, adesc + static_cast<uint64_t>(2 * kk),
+                bdesc + static_cast<uint64_t>((b_kstep >> 4) * kk), idesc,
+                (kb | kk) != 0 ? 1u : 0u);
+    }
+    umma_commit(&sm.bar->empty[sb]);
+    umma_commit(&sm.bar->emptyA[sa]);
+    advance_n<kStagesB>(sb, pb);
+    advance_n<kStagesA>(sa, pa);
   }
 }
 

@@ -15,6 +15,18 @@
 #ifndef FFWD_PRODUCER_WARPS
 #define FFWD_PRODUCER_WARPS 16
 #endif
+// The gathers' fill latency bounds this kernel (no-B timing experiment: 1.78 -> 1.38
+// ms/layer; halving the gathers: -5%), so B gets a 5-deep ring and A a 4-deep one
+// loaded by its own warp (smem 4 x 16 + 5 x 32 KiB).
+#ifndef FFWD_UP_UNSPLIT
+#define FFWD_SPLIT_RING
+#ifndef FFWD_STAGES_A
+#define FFWD_STAGES_A 4
+#endif
+#ifndef FFWD_STAGES_B
+#define FFWD_STAGES_B 5
+#endif
+#endif
 #include "gemm_sm100.cuh"
 
 namespace ffwd {
@@ -68,7 +80,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) {
         uint32_t bytes = contiguous ? 0 : R * BK * 2;
-        if (warp == 0) bytes += kABytes + (contiguous ? UP_BN * BK * 2 : 0);
+        if (warp == 0) bytes += (kSplit ? 0 : kABytes) + (contiguous ? UP_BN * BK * 2 : 0);
         const int r0 = tl.kind != 0 ? 2 * a.f_local + tl.n0 : tl.n0;  // first box row
         const int r1 = tl.kind != 0 ? r0 + 128 : a.f_local + tl.n0;    // second box row
         const int4* rq = reinterpret_cast<const int4*>(rows);
@@ -79,7 +91,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           else
             mbar_arrive(&sm.bar->full[stage]);
           if (warp == 0) {
-            tma_load_2d(&tm_x, &sm.bar->full[stage], sm.a_stage(stage), kb * BK, m.tok0, pol_x);
+            if (!kSplit)
+              tma_load_2d(&tm_x, &sm.bar->full[stage], sm.a_stage(stage), kb * BK, m.tok0,
+                          pol_x);
             if (contiguous) {
               tma_load_2d(&tm_wt, &sm.bar->full[stage], sm.b_stage(stage), kb * BK, r0, pol_w);
               tma_load_2d(&tm_wt, &sm.bar->full[stage], sm.b_stage(stage) + 128 * 128, kb * BK,
@@ -100,17 +114,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       __syncwarp();
     }
+  } else if (kSplit && warp == kAWarp) {
+    // ---------------- A loader (split rings): the block's X tile, one 2-D box per stage
+    if (lane == 0) {
+      const uint64_t pol_x = policy_evict_last();
+      uint32_t sa = 0, pa = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const Tile tl = a.up_tiles[t];
+        if (tl.b < 0) continue;
+        const int tok0 = a.meta[tl.b].tok0;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&sm.bar->emptyA[sa], pa ^ 1);
+          mbar_arrive_expect_tx(&sm.bar->fullA[sa], kABytes);
+          tma_load_2d(&tm_x, &sm.bar->fullA[sa], sm.a_stage(sa), kb * BK, tok0, pol_x);
+          advance_n<kStagesA>(sa, pa);
+        }
+      }
+    }
+    __syncwarp();
   } else if (warp == kMmaWarp) {
     // ---------------- MMA issuer
     constexpr uint32_t idesc = make_idesc_bf16(BM, UP_BN, false, false);
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0, sa = 0, pa = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const Tile tl = a.up_tiles[t];
         if (tl.b < 0) continue;
         mbar_wait_sleep(&sm.bar->tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        mma_tile(sm, tmem + acc * UP_BN, nk, idesc, 16, 1024, 32, stage, phase);
+        if constexpr (kSplit)
+          mma_tile_split(sm, tmem + acc * UP_BN, nk, idesc, 16, 1024, 32, stage, phase, sa, pa);
+        else
+          mma_tile(sm, tmem + acc * UP_BN, nk, idesc, 16, 1024, 32, stage, phase);
         umma_commit(&sm.bar->tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
