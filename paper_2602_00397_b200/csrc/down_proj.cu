@@ -14,6 +14,16 @@
 #ifndef FFWD_PRODUCER_WARPS
 #define FFWD_PRODUCER_WARPS 8
 #endif
+// Split rings as in K2 (A = H on its own loader warp, 4-deep; gathered B 5-deep).
+#ifdef FFWD_DOWN_SPLIT
+#define FFWD_SPLIT_RING
+#ifndef FFWD_STAGES_A
+#define FFWD_STAGES_A 4
+#endif
+#ifndef FFWD_STAGES_B
+#define FFWD_STAGES_B 5
+#endif
+#endif
 #include "gemm_sm100.cuh"
 
 // L2 policies (A/B tuning knobs): 0 evict_normal, 1 evict_first, 2 evict_last.
@@ -92,14 +102,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           mbar_wait(&sm.bar->empty[stage], phase ^ 1);
           uint32_t nbytes = contiguous ? 0 : Q * BN * 2;
-          if (warp == 0) nbytes += kABytes + (contiguous ? BK * BN * 2 : 0);
+          if (warp == 0) nbytes += (kSplit ? 0 : kABytes) + (contiguous ? BK * BN * 2 : 0);
           if (nbytes)
             mbar_arrive_expect_tx(&sm.bar->full[stage], nbytes);
           else
             mbar_arrive(&sm.bar->full[stage]);
           if (warp == 0) {
-            tma_load_2d(&tm_h, &sm.bar->full[stage], sm.a_stage(stage), kb * BK,
-                        tl.b * kBlockTokens, pol_h);
+            if (!kSplit)
+              tma_load_2d(&tm_h, &sm.bar->full[stage], sm.a_stage(stage), kb * BK,
+                          tl.b * kBlockTokens, pol_h);
             if (contiguous) {
               const int r0 = m.idx_row < 0 ? kb * BK : a.f_local + (kb * BK - m.kpad);
 #pragma unroll
@@ -126,17 +137,41 @@ __global__ void __launch_bounds__(kThreads, 1)
         advance(stage, phase);
       }
     }
+  } else if (kSplit && warp == kAWarp) {
+    // ---------------- A loader (split rings): the block's H tile, one 2-D box per stage
+    if (lane == 0) {
+      const uint64_t pol_h = FFWD_K3_H_POLICY == 2 ? policy_evict_last()
+                                                   : policy_evict_normal();
+      uint32_t sa = 0, pa = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const Tile tl = a.down_tiles[t];
+        if (tl.b < 0) continue;
+        const int nk = a.meta[tl.b].ktot / BK;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&sm.bar->emptyA[sa], pa ^ 1);
+          mbar_arrive_expect_tx(&sm.bar->fullA[sa], kABytes);
+          tma_load_2d(&tm_h, &sm.bar->fullA[sa], sm.a_stage(sa), kb * BK, tl.b * kBlockTokens,
+                      pol_h);
+          advance_n<kStagesA>(sa, pa);
+        }
+      }
+    }
+    __syncwarp();
   } else if (warp == kMmaWarp) {
     constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, true);
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0, sa = 0, pa = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const Tile tl = a.down_tiles[t];
         if (tl.b < 0) continue;
         const BlockMeta m = a.meta[tl.b];
         mbar_wait_sleep(&sm.bar->tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        mma_tile(sm, tmem + acc * BN, m.ktot / BK, idesc, kLbo, 1024, 2048, stage, phase);
+        if constexpr (kSplit)
+          mma_tile_split(sm, tmem + acc * BN, m.ktot / BK, idesc, kLbo, 1024, 2048, stage, phase,
+                         sa, pa);
+        else
+          mma_tile(sm, tmem + acc * BN, m.ktot / BK, idesc, kLbo, 1024, 2048, stage, phase);
         umma_commit(&sm.bar->tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
