@@ -358,6 +358,12 @@ def run_gpu(args, rank: int, world: int) -> None:
 
     gain = torch.ones(d, device=dev)            # ffn_norm gains (ones, synthetic.py:41)
     lg = torch.empty((T,), dtype=torch.float32, device=dev)
+    peers = None
+    if tp > 1 and args.collective == "fused":
+        # fused completion: partial Y -> peer-memory reduce + residual add (tp.PeerBuffers)
+        from paper_2602_00397_b200.tp import PeerBuffers
+        peers = PeerBuffers(T, d, dev, with_xnext=False)
+        res = peers.out
 
     def stack(x_src: torch.Tensor):
         # engine.py:267-308 per layer: x = rmsnorm(h, ffn_norm) (fused with the predictor's
@@ -368,6 +374,10 @@ def run_gpu(args, rank: int, world: int) -> None:
             if tp == 1:
                 ff.sparse_ffn_layer(xb, packed, dp, k, out=res, residual=res, logits_in=lg,
                                     workspace=ws)
+            elif peers is not None:
+                ff.sparse_ffn_layer(xb, packed, dp, k, out=peers.partial, logits_in=lg,
+                                    workspace=ws)
+                peers.complete(res)
             else:
                 ff.sparse_ffn_layer(xb, packed, dp, k, out=ybuf, logits_in=lg, workspace=ws)
                 torch.distributed.all_reduce(ybuf)
@@ -456,6 +466,7 @@ def run_gpu(args, rank: int, world: int) -> None:
                    else ks[0], "block": 128, "dense_first_last": True,
                    "parallelism": f"tp{tp}" if tp > 1 else (f"dp{world}" if world > 1
                                                             else "single"),
+                   "collective": args.collective if tp > 1 else None,
                    "l2": "inputs larger than L2 (X 128 MiB, 361 MiB weights per layer, "
                          "32 distinct layers per step); no flush"},
         "e2e": {"value": e2e_ms / L, "unit": "ms/layer", "h2d_bytes_per_step": h2d,
@@ -531,6 +542,8 @@ def main():
     ap.add_argument("--skip-dense", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-ttft", action="store_true")
+    ap.add_argument("--collective", default="nccl", choices=["nccl", "fused"],
+                    help="TP completion: NCCL all-reduce, or the fused peer-memory kernel")
     ap.add_argument("--parallel", default="tp", choices=["tp", "dp"],
                     help="N>1: tensor parallel over d_ffn (one prompt) or data parallel "
                          "(one prompt per GPU)")

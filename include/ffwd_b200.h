@@ -227,6 +227,31 @@ FFWD_API int ffwd_ckpt_tensor(void* handle, int i, const char** name, int* ndim,
                               const float** data, uint64_t* nbytes);
 
 /*
+ * Tensor-parallel completion of the down projection over NVLink peer memory, fused
+ * with the residual add (engine.py:308): for this rank's row slice
+ * [T*rank/n, T*(rank+1)/n) it reads every rank's partial Y from that rank's HBM,
+ * adds the local residual rows and writes the result (and, if xnexts != NULL, its
+ * bf16 copy) into every rank's output -- reduce-scatter + all-gather in one pass.
+ * Host arrays of n device pointers (peer pointers from ffwd_ipc_open):
+ *   partials[p]  f32 [T x d] rank p's partial Y (written by its down projection);
+ *   outs[p]      f32 [T x d] rank p's residual stream (may alias its residual);
+ *   xnexts[p]    bf16 [T x d] or NULL;
+ *   flags[p]     u32 [2n + 1] zero-initialised sync words of rank p.
+ * `epoch` must increase by one per call (flags are never reset).  Cross-GPU waits
+ * are bounded and trap instead of hanging.  max_ctas <= 0: one CTA per SM (the grid
+ * must be co-resident).
+ */
+FFWD_API int ffwd_allreduce_residual(const float* const* partials, float* const* outs,
+                                     void* const* xnexts, unsigned* const* flags, int n_ranks,
+                                     int rank, const float* residual, int T, int d,
+                                     unsigned epoch, int max_ctas, void* stream);
+/* CUDA IPC: the 64-byte handle of the allocation holding dev_ptr plus dev_ptr's
+ * offset in it; ffwd_ipc_open maps a peer's allocation (add the offset). */
+FFWD_API int ffwd_ipc_get_handle(void* dev_ptr, void* handle_out, size_t* offset_out);
+FFWD_API int ffwd_ipc_open(const void* handle, void** dev_ptr);
+FFWD_API int ffwd_ipc_close(void* dev_ptr);
+
+/*
  * Per-launch device timing (CUDA events on the launching stream) for the
  * measurement harness.  Stages: 0 pool, 1 predictor W1, 2 predictor W2,
  * 3 top-k, 4 plan, 5 up-projection (K2), 6 down-projection (K3), 7 FFN-input

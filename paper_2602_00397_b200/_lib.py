@@ -64,6 +64,11 @@ SIGNATURES = {
     "ffwd_ckpt_tensor": (_c_int, [_vp, _c_int, ctypes.POINTER(ctypes.c_char_p),
                                   ctypes.POINTER(_c_int), ctypes.POINTER(ctypes.c_uint32),
                                   ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_uint64)]),
+    "ffwd_allreduce_residual": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _vp, _c_int, _c_int,
+                                         ctypes.c_uint, _c_int, _vp]),
+    "ffwd_ipc_get_handle": (_c_int, [_vp, _vp, ctypes.POINTER(_c_size)]),
+    "ffwd_ipc_open": (_c_int, [_vp, ctypes.POINTER(_vp)]),
+    "ffwd_ipc_close": (_c_int, [_vp]),
     "ffwd_timing_enable": (_c_int, [_c_int]),
     "ffwd_timing_read": (_c_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_c_int),
                                   _c_int]),

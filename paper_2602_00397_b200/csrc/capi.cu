@@ -2,7 +2,10 @@
 // error semantics, workspace carving, and the per-layer launch sequence
 //   pool -> W1 -> W2 -> top-k -> plan -> up-proj (K2) -> down-proj (K3).
 #include <cuda_bf16.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
+
+#include <cstring>
 
 #include <algorithm>
 #include <cmath>
@@ -580,6 +583,66 @@ int ffwd_ffn_layer_mode(const void* x_bf16, int T, int d, const void* wgu_t, con
   Ffn w = carve_ffn(c2, T, d, f, rc_local, k, 0, 4);
   return run_ffn(x_bf16, T, d, wgu_t, wd, f, rc_local, w, idx, ld, b0, nb, nullptr, k,
                  mode == 2 ? 1 : 0, has_comp, y, residual, x_next_bf16, s);
+}
+
+int ffwd_ipc_get_handle(void* dev_ptr, void* handle_out, size_t* offset_out) {
+  g_err.clear();
+  // the handle names the whole allocation; the opener adds this pointer's offset
+  using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static RangeFn range = nullptr;
+  if (!range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess)
+      return fail(FFWD_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    range = reinterpret_cast<RangeFn>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+    return fail(FFWD_ERR_CUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  FFWD_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle");
+  std::memcpy(handle_out, &h, sizeof(h));
+  *offset_out = static_cast<size_t>(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  return FFWD_OK;
+}
+
+int ffwd_ipc_open(const void* handle, void** dev_ptr) {
+  g_err.clear();
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  FFWD_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess),
+            "cudaIpcOpenMemHandle");
+  return FFWD_OK;
+}
+
+int ffwd_ipc_close(void* dev_ptr) {
+  g_err.clear();
+  FFWD_CUDA(cudaIpcCloseMemHandle(dev_ptr), "cudaIpcCloseMemHandle");
+  return FFWD_OK;
+}
+
+int ffwd_allreduce_residual(const float* const* partials, float* const* outs,
+                            void* const* xnexts, unsigned* const* flags, int n_ranks, int rank,
+                            const float* residual, int T, int d, unsigned epoch, int max_ctas,
+                            void* stream) {
+  g_err.clear();
+  if (n_ranks < 1 || n_ranks > 8 || rank < 0 || rank >= n_ranks)
+    return fail(FFWD_ERR_VALIDATION, "bad rank %d of %d (1..8 ranks)", rank, n_ranks);
+  if (T < 1 || d < 4 || d % 4 != 0)
+    return fail(FFWD_ERR_VALIDATION, "allreduce dims T=%d d=%d (d %% 4 == 0)", T, d);
+  if (!partials || !outs || !flags || !residual)
+    return fail(FFWD_ERR_VALIDATION, "allreduce needs partial, out, flag and residual pointers");
+  for (int p = 0; p < n_ranks; ++p)
+    if (!partials[p] || !outs[p] || !flags[p] || (xnexts && !xnexts[p]))
+      return fail(FFWD_ERR_VALIDATION, "null peer pointer for rank %d", p);
+  const int ctas = max_ctas > 0 ? max_ctas : num_sms();
+  FFWD_CUDA(launch_allreduce_residual(partials, outs, xnexts, flags, n_ranks, rank, residual, T,
+                                      d, epoch, ctas, static_cast<cudaStream_t>(stream)),
+            "allreduce_residual");
+  return FFWD_OK;
 }
 
 int ffwd_rmsnorm(float* x, const float* gain, int T, int d, double eps, const void* add,

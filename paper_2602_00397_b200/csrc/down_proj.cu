@@ -160,7 +160,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kMmaWarp) {
     constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, true);
     if (lane == 0) {
-      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0, sa = 0, pa = 0;
+      uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
+      [[maybe_unused]] uint32_t sa = 0, pa = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const Tile tl = a.down_tiles[t];
         if (tl.b < 0) continue;

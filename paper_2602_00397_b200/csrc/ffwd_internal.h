@@ -50,6 +50,12 @@ cudaError_t launch_rmsnorm(float* x, const float* gain, int T, int d, double eps
                            const void* add, int add_kind, void* out_bf16, float* out_f32,
                            const float* query, float sqrt_d, float* logits, int logit_row0,
                            int logit_row1, cudaStream_t s);
+// Fused tensor-parallel completion (allreduce.cu): out_p = residual + sum_q partial_q on
+// every rank p (peer pointers), optional bf16 copy; flags: per-rank [2n + 1] words.
+cudaError_t launch_allreduce_residual(const float* const* partial, float* const* out,
+                                      void* const* xnext, unsigned* const* flags, int n,
+                                      int rank, const float* residual, int T, int d,
+                                      unsigned epoch, int max_ctas, cudaStream_t s);
 // sparse.hidden_column_scores over bf16 H [n_blk*128 x hcols] -> scores [n_blk x f]
 cudaError_t launch_hidden_scores(const void* h, bool is_f32, int ld, int T, int f,
                                  float* scores, cudaStream_t s);

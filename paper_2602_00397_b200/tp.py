@@ -6,7 +6,10 @@ contiguous 1/N slice of the compensator bottleneck.  The predictor is
 replicated: every rank computes the same global top-k (bit-exact, so no
 collective is needed before the FFN) and keeps its local subset.  Each rank's
 down projection yields a partial Y; one all-reduce (sum) per layer completes
-it.  Independent prompts are data parallel and need no collective at all.
+it -- either NCCL (``allreduce_partial``) or the fused peer-memory kernel
+(``PeerBuffers.complete``: reduce-scatter + all-gather over NVLink in one pass,
+with the residual add and the next layer's bf16 input fused in).  Independent
+prompts are data parallel and need no collective at all.
 """
 
 from __future__ import annotations
@@ -79,3 +82,96 @@ class TensorParallelFFN:
         y = sparse_ffn_layer(x, self.packed, self.predictor, self.k,
                              dense_first_last=self.dense_first_last, out=out)
         return allreduce_partial(y, self.group)
+
+
+# ---------------------------------------------------------------- fused completion
+def allreduce_residual_fused(partials, outs, flags, rank: int, residual: torch.Tensor,
+                             epoch: int, xnexts=None, max_ctas: int = 0) -> None:
+    """One rank's fused TP completion (``ffwd_allreduce_residual``): for its row slice,
+    out_p = residual + sum_q partial_q on every rank p, over peer pointers.
+
+    ``partials`` / ``outs`` / ``flags`` / ``xnexts``: one entry per rank, each a CUDA
+    tensor (single-process emulation) or an int device pointer (peer mappings from
+    ``PeerBuffers``).  ``epoch`` increases by one per call.
+    """
+    import ctypes
+    from . import _dev, _lib
+    n = len(partials)
+    if not (len(outs) == len(flags) == n) or (xnexts is not None and len(xnexts) != n):
+        raise ValidationError("one partial, out, flag (and x_next) buffer per rank")
+    T, d = residual.shape
+
+    def ptrs(items):
+        arr = (ctypes.c_void_p * n)()
+        for i, t in enumerate(items):
+            arr[i] = t if isinstance(t, int) else t.data_ptr()
+        return arr
+
+    lib = _dev.lib_for(residual.device)
+    _lib.check(lib.ffwd_allreduce_residual(
+        ptrs(partials), ptrs(outs), ptrs(xnexts) if xnexts is not None else None, ptrs(flags),
+        n, rank, residual.data_ptr(), T, d, int(epoch) & 0xFFFFFFFF, max_ctas,
+        _dev.stream_handle(residual.device)), "allreduce_residual")
+
+
+class PeerBuffers:
+    """Per-rank partial-Y, residual-stream and flag buffers shared over CUDA IPC, for the
+    fused TP completion (one process per GPU, NVLink peer access)."""
+
+    def __init__(self, T: int, d: int, device, group=None, with_xnext: bool = True):
+        import ctypes
+        from . import _lib
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        dev = torch.device(device)
+        self.partial = torch.empty((T, d), dtype=torch.float32, device=dev)
+        self.out = torch.empty((T, d), dtype=torch.float32, device=dev)
+        self.xnext = torch.empty((T, d), dtype=torch.bfloat16, device=dev) if with_xnext else None
+        self.flags = torch.zeros((2 * self.world + 1,), dtype=torch.int32, device=dev)
+        lib = _lib.load_library()
+        mine = []
+        for t in (self.partial, self.out, self.xnext, self.flags):
+            if t is None:
+                mine.append(None)
+                continue
+            h = (ctypes.c_char * 64)()
+            off = ctypes.c_size_t()
+            _lib.check(lib.ffwd_ipc_get_handle(t.data_ptr(), h, ctypes.byref(off)), "ipc handle")
+            mine.append((bytes(h), off.value))
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        self._opened = []
+        self.peer = {"partial": [], "out": [], "xnext": [], "flags": []}
+        for p in range(self.world):
+            for key, t, hv in zip(("partial", "out", "xnext", "flags"),
+                                  (self.partial, self.out, self.xnext, self.flags), allh[p]):
+                if hv is None:
+                    continue
+                if p == self.rank:
+                    self.peer[key].append(t.data_ptr())
+                    continue
+                base = ctypes.c_void_p()
+                _lib.check(lib.ffwd_ipc_open(hv[0], ctypes.byref(base)), "ipc open")
+                self._opened.append(base.value)
+                self.peer[key].append(base.value + hv[1])
+        self.epoch = 0
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)
+
+    def complete(self, residual: torch.Tensor, max_ctas: int = 0) -> torch.Tensor:
+        """After this rank's down projection wrote ``self.partial``: every rank's ``out``
+        becomes residual + sum of partials (and ``xnext`` its bf16 copy)."""
+        self.epoch += 1
+        allreduce_residual_fused(self.peer["partial"], self.peer["out"], self.peer["flags"],
+                                 self.rank, residual, self.epoch,
+                                 self.peer["xnext"] if self.xnext is not None else None,
+                                 max_ctas)
+        return self.out
+
+    def close(self):
+        from . import _lib
+        lib = _lib.load_library()
+        for p in self._opened:
+            lib.ffwd_ipc_close(p)
+        self._opened = []
