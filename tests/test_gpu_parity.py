@@ -141,6 +141,22 @@ def test_dense_layer_and_full_k_shortcut(ff):
     assert_close(y.cpu().numpy(), want, "full-k layer")
 
 
+def test_full_mask_is_bit_identical_to_dense(ff):
+    """Acceptance criterion 1's second half (test_sparse.py:107-115): the gathered FFN
+    with every neuron selected equals the dense FFN bit for bit -- the gather4 path
+    (explicit ascending index) and the 2-D tile path (identity) stage identical bytes."""
+    c, packed, _ = _layer_case(ff, "cfg1")
+    x = torch.from_numpy(c["x"]).to("cuda", torch.bfloat16)
+    f = c["f"]
+    n_blk = -(-x.shape[0] // 128)
+    ld = -(-f // 4) * 4
+    idx = torch.zeros((n_blk, ld), dtype=torch.int32, device="cuda")
+    idx[:, :f] = torch.arange(f, dtype=torch.int32, device="cuda")
+    y_gather = ff.run_sparse_ffn(x, packed, idx, f, has_comp=False)
+    y_dense = ff.dense_ffn(x, packed)
+    assert torch.equal(y_gather, y_dense)
+
+
 def test_reference_api_drop_in(ff):
     """predictor_forward / build_mask / select_subweights / sparse_ffn_forward /
     compensator_forward with numpy in, numpy out (engine.py:286-300 call pattern)."""
