@@ -59,8 +59,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < kProducerWarps) {
     // ---------------- producers: warp w gathers B rows [R w, R w + R) of every stage
     constexpr int R = UP_BN / kProducerWarps;  // rows per producer warp
+#ifndef FFWD_K2_W_POLICY
+#define FFWD_K2_W_POLICY 0
+#endif
     const uint64_t pol_x = policy_evict_last();
-    const uint64_t pol_w = policy_evict_normal();
+    const uint64_t pol_w = FFWD_K2_W_POLICY == 2 ? policy_evict_last()
+                           : FFWD_K2_W_POLICY == 1 ? policy_evict_first() : policy_evict_normal();
     int* rows = sm.bar->rows[warp];
     uint32_t stage = 0, phase = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -117,7 +121,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (kSplit && warp == kAWarp) {
     // ---------------- A loader (split rings): the block's X tile, one 2-D box per stage
     if (lane == 0) {
-      const uint64_t pol_x = policy_evict_last();
+#ifndef FFWD_K2_X_POLICY
+#define FFWD_K2_X_POLICY 2
+#endif
+      const uint64_t pol_x = FFWD_K2_X_POLICY == 2 ? policy_evict_last()
+                             : FFWD_K2_X_POLICY == 1 ? policy_evict_first() : policy_evict_normal();
       uint32_t sa = 0, pa = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const Tile tl = a.up_tiles[t];
