@@ -205,11 +205,13 @@ FFWD_API int ffwd_rmsnorm(float* x, const float* gain, int T, int d, double eps,
  * buffer (bf16, or f32 when is_f32): Q heads at columns [0, n_heads*d_head),
  * K heads at [k_col, k_col + n_heads*d_head).  Token t sits at position
  * pos0 + t; cos_t / sin_t are f64 [max_pos x d_head/2] tables of
- * cos/sin(pos * 10000^(-2i/d_head)).
+ * cos/sin(pos * 10000^(-2i/d_head)).  f32 storage is rotated in f64 (bit-exact to
+ * the reference); bf16 storage in f32 from cos32 / sin32 (f32 copies of the tables;
+ * NULL = the f64 path).
  */
 FFWD_API int ffwd_rope(void* qk, int is_f32, int T, int row_stride, int k_col, int n_heads,
-                       int d_head, const double* cos_t, const double* sin_t, int pos0,
-                       void* stream);
+                       int d_head, const double* cos_t, const double* sin_t, const float* cos32,
+                       const float* sin32, int pos0, void* stream);
 
 /*
  * `.ffwd` checkpoint reader (checkpoint.py:1-22 layout, read_checkpoint :207-263):

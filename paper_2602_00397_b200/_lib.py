@@ -54,8 +54,8 @@ SIGNATURES = {
                                      _c_size, _vp]),
     "ffwd_rmsnorm": (_c_int, [_vp, _vp, _c_int, _c_int, ctypes.c_double, _vp, _c_int, _vp, _vp,
                               _vp, _vp, _c_int, _c_int, _vp]),
-    "ffwd_rope": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp,
-                           _c_int, _vp]),
+    "ffwd_rope": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp,
+                           _vp, _c_int, _vp]),
     "ffwd_ckpt_last_error": (ctypes.c_char_p, []),
     "ffwd_ckpt_open": (_c_int, [ctypes.c_char_p, ctypes.POINTER(_vp)]),
     "ffwd_ckpt_close": (None, [_vp]),

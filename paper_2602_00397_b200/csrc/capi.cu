@@ -669,7 +669,8 @@ int ffwd_rmsnorm(float* x, const float* gain, int T, int d, double eps, const vo
 }
 
 int ffwd_rope(void* qk, int is_f32, int T, int row_stride, int k_col, int n_heads, int d_head,
-              const double* cos_t, const double* sin_t, int pos0, void* stream) {
+              const double* cos_t, const double* sin_t, const float* cos32, const float* sin32,
+              int pos0, void* stream) {
   g_err.clear();
   if (T < 1 || n_heads < 1 || d_head < 4 || d_head % 4 != 0)
     return fail(FFWD_ERR_VALIDATION, "rope dims T=%d heads=%d d_head=%d (d_head %% 4 == 0)", T,
@@ -679,7 +680,7 @@ int ffwd_rope(void* qk, int is_f32, int T, int row_stride, int k_col, int n_head
                 k_col, n_heads, d_head);
   if (pos0 < 0) return fail(FFWD_ERR_VALIDATION, "rope pos0=%d < 0", pos0);
   FFWD_CUDA(launch_rope(qk, is_f32 != 0, T, row_stride, k_col, n_heads, d_head, cos_t, sin_t,
-                        pos0, static_cast<cudaStream_t>(stream)),
+                        cos32, sin32, pos0, static_cast<cudaStream_t>(stream)),
             "rope");
   return FFWD_OK;
 }

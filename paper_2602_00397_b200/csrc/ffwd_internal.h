@@ -60,8 +60,8 @@ cudaError_t launch_allreduce_residual(const float* const* partial, float* const*
 cudaError_t launch_hidden_scores(const void* h, bool is_f32, int ld, int T, int f,
                                  float* scores, cudaStream_t s);
 cudaError_t launch_rope(void* qk, bool is_f32, int T, int row_stride, int k_col, int n_heads,
-                        int d_head, const double* cos_t, const double* sin_t, int pos0,
-                        cudaStream_t s);
+                        int d_head, const double* cos_t, const double* sin_t, const float* cos32,
+                        const float* sin32, int pos0, cudaStream_t s);
 // `partial` (nullable, gemm_f64acc_partial_bytes) enables split-K.
 size_t gemm_f64acc_partial_bytes(int M, int K, int N);
 cudaError_t launch_gemm_f64acc(const float* A, const float* B, float* C, int M, int K, int N,

@@ -10,8 +10,9 @@
 //                   predictor's first pass over X disappears.
 //   rope_kernel     rotary embedding of Q and K in place (engine.py:50-68 apply_rope):
 //                   each head's (first half, second half) pairs rotated by the
-//                   position angle, products in f64 from an f64 cos/sin table, one
-//                   rounding to the storage type.
+//                   position angle: f32 storage in f64 from an f64 cos/sin table (one
+//                   rounding, bit-exact to the reference); bf16 storage in f32 from f32
+//                   copies of the table.
 //
 // Both are HBM bound: RMSNorm reads 4 B and writes 2 (+4) B per element, RoPE reads
 // and writes Q and K once.
@@ -162,7 +163,8 @@ __global__ void __launch_bounds__(kNormThreads, 2)
 template <typename E>
 __global__ void __launch_bounds__(256)
     rope_kernel(E* __restrict__ qk, int row_stride, int k_col, int n_heads, int d_head,
-                const double* __restrict__ cos_t, const double* __restrict__ sin_t, int pos0) {
+                const double* __restrict__ cos_t, const double* __restrict__ sin_t,
+                const float* __restrict__ cos32, const float* __restrict__ sin32, int pos0) {
   using E2 = std::conditional_t<std::is_same_v<E, float>, float2, __nv_bfloat162>;
   const int t = blockIdx.x;
   const int half = d_head / 2;
@@ -185,13 +187,26 @@ __global__ void __launch_bounds__(256)
       a0 = fa.x; a1 = fa.y; b0 = fb.x; b1 = fb.y;
     }
     float o[4];
-    const double xs1[2] = {a0, a1}, xs2[2] = {b0, b1};
+    if (cos32 != nullptr) {
+      // bf16 storage: f32 arithmetic from f32 tables (the bf16 rounding dominates; F2F-free)
+      const float* c32 = cos32 + static_cast<size_t>(pos0 + t) * half;
+      const float* s32 = sin32 + static_cast<size_t>(pos0 + t) * half;
+      const float xs1[2] = {a0, a1}, xs2[2] = {b0, b1};
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const double c = __ldg(ct + i + e), sn = __ldg(st + i + e);
-      // engine.py:65-66, each f64 product and sum rounded separately (no contraction)
-      o[e] = static_cast<float>(__dsub_rn(__dmul_rn(xs1[e], c), __dmul_rn(xs2[e], sn)));
-      o[2 + e] = static_cast<float>(__dadd_rn(__dmul_rn(xs1[e], sn), __dmul_rn(xs2[e], c)));
+      for (int e = 0; e < 2; ++e) {
+        const float c = __ldg(c32 + i + e), sn = __ldg(s32 + i + e);
+        o[e] = xs1[e] * c - xs2[e] * sn;
+        o[2 + e] = xs1[e] * sn + xs2[e] * c;
+      }
+    } else {
+      const double xs1[2] = {a0, a1}, xs2[2] = {b0, b1};
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double c = __ldg(ct + i + e), sn = __ldg(st + i + e);
+        // engine.py:65-66, each f64 product and sum rounded separately (no contraction)
+        o[e] = static_cast<float>(__dsub_rn(__dmul_rn(xs1[e], c), __dmul_rn(xs2[e], sn)));
+        o[2 + e] = static_cast<float>(__dadd_rn(__dmul_rn(xs1[e], sn), __dmul_rn(xs2[e], c)));
+      }
     }
     if constexpr (std::is_same_v<E, float>) {
       *p1 = make_float2(o[0], o[1]);
@@ -245,19 +260,20 @@ cudaError_t launch_rmsnorm(float* x, const float* gain, int T, int d, double eps
 }
 
 cudaError_t launch_rope(void* qk, bool is_f32, int T, int row_stride, int k_col, int n_heads,
-                        int d_head, const double* cos_t, const double* sin_t, int pos0,
-                        cudaStream_t s) {
+                        int d_head, const double* cos_t, const double* sin_t, const float* cos32,
+                        const float* sin32, int pos0, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   const dim3 grid(T);
   const int units = n_heads * (d_head / 2);  // 2 x n_heads x (d_head / 4)
   const int threads = units >= 256 ? 256 : (units + 31) / 32 * 32;
   if (is_f32)
     rope_kernel<float><<<grid, threads, 0, s>>>(static_cast<float*>(qk), row_stride, k_col,
-                                                n_heads, d_head, cos_t, sin_t, pos0);
+                                                n_heads, d_head, cos_t, sin_t, nullptr, nullptr,
+                                                pos0);
   else
     rope_kernel<__nv_bfloat16><<<grid, threads, 0, s>>>(static_cast<__nv_bfloat16*>(qk),
                                                         row_stride, k_col, n_heads, d_head,
-                                                        cos_t, sin_t, pos0);
+                                                        cos_t, sin_t, cos32, sin32, pos0);
   return cudaGetLastError();
 }
 

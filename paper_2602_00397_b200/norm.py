@@ -68,8 +68,9 @@ def rmsnorm(x: torch.Tensor, gain: torch.Tensor, eps: float = 1e-6, out_bf16: bo
 _rope_cache: dict = {}
 
 
-def rope_tables(n_pos: int, d_head: int, device) -> tuple[torch.Tensor, torch.Tensor]:
-    """f64 cos/sin tables [n_pos x d_head/2] with the reference's formula (engine.py:59-62)."""
+def rope_tables(n_pos: int, d_head: int, device) -> tuple:
+    """cos/sin tables [n_pos x d_head/2] with the reference's formula (engine.py:59-62):
+    (cos f64, sin f64, cos f32, sin f32)."""
     dev = torch.device(device)
     key = (str(dev), d_head)
     hit = _rope_cache.get(key)
@@ -78,7 +79,8 @@ def rope_tables(n_pos: int, d_head: int, device) -> tuple[torch.Tensor, torch.Te
     half = d_head // 2
     freqs = ROPE_BASE ** (-2.0 * np.arange(half) / d_head)
     ang = np.arange(n_pos)[:, None].astype(np.float64) * freqs[None, :]
-    tabs = (torch.from_numpy(np.cos(ang)).to(dev), torch.from_numpy(np.sin(ang)).to(dev))
+    c64, s64 = torch.from_numpy(np.cos(ang)).to(dev), torch.from_numpy(np.sin(ang)).to(dev)
+    tabs = (c64, s64, c64.float(), s64.float())
     _rope_cache[key] = tabs
     return tabs
 
@@ -92,9 +94,12 @@ def apply_rope(qkv: torch.Tensor, n_heads: int, d_head: int, pos0: int = 0,
     T, stride = qkv.shape
     d = n_heads * d_head
     kc = d if k_col is None else k_col
-    cos_t, sin_t = rope_tables(pos0 + T, d_head, qkv.device)
+    cos_t, sin_t, cos32, sin32 = rope_tables(pos0 + T, d_head, qkv.device)
+    is_f32 = qkv.dtype == torch.float32
     lib = _dev.lib_for(qkv.device)
-    _lib.check(lib.ffwd_rope(qkv.data_ptr(), int(qkv.dtype == torch.float32), T, stride, kc,
-                             n_heads, d_head, cos_t.data_ptr(), sin_t.data_ptr(), pos0,
+    _lib.check(lib.ffwd_rope(qkv.data_ptr(), int(is_f32), T, stride, kc, n_heads, d_head,
+                             cos_t.data_ptr(), sin_t.data_ptr(),
+                             None if is_f32 else cos32.data_ptr(),
+                             None if is_f32 else sin32.data_ptr(), pos0,
                              _dev.stream_handle(qkv.device)), "rope")
     return qkv

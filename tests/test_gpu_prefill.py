@@ -113,6 +113,26 @@ def test_rope_f32_bit_exact(ff, T, H, dh, pos0):
     assert np.array_equal(got[:, 2 * d:], qkv[:, 2 * d:])  # V untouched
 
 
+def test_rope_bf16_matches_reference_rounding(ff):
+    """bf16 storage rotates in f32: equal to bf16(reference f32 result) except for
+    <= 0.1% of elements (rounding ties; cancellation in x1 c - x2 s), off by <= 4 bf16 ulp."""
+    from paper_2602_00397_b200.norm import apply_rope
+    T, H, dh = 300, 8, 128
+    d = H * dh
+    rng = np.random.default_rng(9)
+    qkv = orc.bf16_round(rng.standard_normal((T, 3 * d)).astype(np.float32))
+    got = apply_rope(torch.from_numpy(qkv).cuda().to(torch.bfloat16), H, dh, pos0=50)
+    got = got.float().cpu().numpy()
+    for lo in (0, d):
+        want = orc.bf16_round(rope_ref(qkv[:, lo:lo + d], H, dh, 50))
+        diff = got[:, lo:lo + d] != want
+        assert diff.mean() <= 1e-3
+        if diff.any():
+            ulp = np.abs(got[:, lo:lo + d][diff].view(np.int32) - want[diff].view(np.int32))
+            assert ulp.max() <= 4 << 16  # bf16 ulps in the f32 bit pattern
+    assert np.array_equal(got[:, 2 * d:], qkv[:, 2 * d:])
+
+
 def _device_model(ff, c, attn_dtype):
     from paper_2602_00397_b200.model import LayerWeights, ModelConfig, ModelWeights
     from paper_2602_00397_b200.prefill import DeviceModel
