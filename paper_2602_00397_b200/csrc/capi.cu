@@ -23,7 +23,7 @@ namespace {
 
 thread_local std::string g_err;
 int g_up_group = 32;
-int g_down_group = 8;
+int g_down_group = 16;  // ncu sweep: K3 DRAM 3.0 GB -> 1.7 GB per layer vs 8 (profiles/r1_raster_sweep.txt)
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];

@@ -8,6 +8,8 @@ import paper_2602_00397_b200 as ff
 cfg = sys.argv[1] if len(sys.argv) > 1 else "8b"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 mode = sys.argv[3] if len(sys.argv) > 3 else "sparse"
+if len(sys.argv) > 4:  # raster groups "UP,DOWN"
+    ff.set_raster(*(int(v) for v in sys.argv[4].split(",")))
 d, f, L, T, keep = bench.CONFIGS[cfg]
 bench.CONFIGS[cfg] = (d, f, 1, T, keep)
 dev = torch.device("cuda", 0)
