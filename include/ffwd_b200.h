@@ -57,6 +57,9 @@ FFWD_API int ffwd_device_check(int device);
 
 /* Tuning knobs of the gather-GEMM rasterisation (blocks per L2 group). */
 FFWD_API int ffwd_set_raster(int up_group, int down_group);
+/* Tuning knob: odd up-projection raster groups sweep their neuron tiles downwards (1,
+ * default) so the previous group's last weight rows are still in L2. */
+FFWD_API int ffwd_set_serpentine(int on);
 
 /*
  * Predictor scores for blocks [blk_begin, blk_begin + blk_count) of x.

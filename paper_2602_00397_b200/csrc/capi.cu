@@ -23,6 +23,7 @@ namespace {
 
 thread_local std::string g_err;
 int g_up_group = 32;
+int g_serpentine = 1;
 int g_down_group = 16;  // ncu sweep: K3 DRAM 3.0 GB -> 1.7 GB per layer vs 8 (profiles/r1_raster_sweep.txt)
 
 int fail(int code, const char* fmt, ...) {
@@ -220,6 +221,7 @@ int run_ffn(const void* x, int T, int d, const void* wgu_t, const void* wd, int 
   pa.down_group = g_down_group;
   pa.bn_down = bn_for(d);
   pa.hcols_alloc = w.hcols;
+  pa.serpentine = g_serpentine;
   {
     StageTimer tm(kPlan, s);
     FFWD_CUDA(launch_plan(pa, w.meta, w.up, w.up_cap, w.down, w.down_cap, w.pc, s), "plan");
@@ -283,6 +285,11 @@ int ffwd_device_check(int device) {
   if (p.major != 10 || p.minor != 0)
     return fail(FFWD_ERR_UNSUPPORTED, "device %d is sm_%d%d; kernels are built for sm_100a",
                 device, p.major, p.minor);
+  return FFWD_OK;
+}
+
+int ffwd_set_serpentine(int on) {
+  g_serpentine = on != 0;
   return FFWD_OK;
 }
 

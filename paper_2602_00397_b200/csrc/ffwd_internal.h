@@ -83,6 +83,7 @@ struct PlanArgs {
   int down_group;                  // blocks per raster group (down projection)
   int bn_down;                     // output columns per down tile
   int hcols_alloc;
+  int serpentine;                  // odd up-projection raster groups sweep tiles downwards
 };
 
 cudaError_t launch_plan(const PlanArgs& a, BlockMeta* meta, Tile* up_tiles, int up_cap,

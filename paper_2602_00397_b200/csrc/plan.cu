@@ -99,7 +99,12 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
     const int o1 = min(lo < g_dense ? n_dense : a.n_blk, o0 + a.up_group);
     const int sz = o1 - o0;
     const int rel = slot - s_gbase[lo];
-    const int i = rel / sz, o = o0 + rel % sz;
+    const int mx = (s_gbase[lo + 1] - s_gbase[lo]) / sz;  // tiles per block in this group
+    int i = rel / sz;
+    const int o = o0 + rel % sz;
+    // serpentine: odd groups sweep the neuron tiles downwards, so the weight rows the
+    // previous group touched last are still in L2 when the next group starts
+    if (a.serpentine && (lo & 1)) i = mx - 1 - i;
     Tile t{-1, 0, 0, 0};
     if (i < s_ngu[o]) {
       t = Tile{order_to_block(o, a), i * 128, 0, 0};

@@ -10,6 +10,9 @@ iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 mode = sys.argv[3] if len(sys.argv) > 3 else "sparse"
 if len(sys.argv) > 4:  # raster groups "UP,DOWN"
     ff.set_raster(*(int(v) for v in sys.argv[4].split(",")))
+if len(sys.argv) > 5:  # serpentine 0/1
+    from paper_2602_00397_b200 import _lib
+    _lib.load_library().ffwd_set_serpentine(int(sys.argv[5]))
 d, f, L, T, keep = bench.CONFIGS[cfg]
 bench.CONFIGS[cfg] = (d, f, 1, T, keep)
 dev = torch.device("cuda", 0)
