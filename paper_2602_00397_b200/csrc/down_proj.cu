@@ -80,8 +80,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (tl.b < 0) continue;
       const BlockMeta m = a.meta[tl.b];
       const int nk = m.ktot / BK;
+      // Tile.pad = 1: this tile walks its K stages from the top down (serpentine raster:
+      // the W_down rows the previous group read last are still in L2)
+      auto kidx = [&](int kb) { return tl.pad ? nk - 1 - kb : kb; };
       auto row_of = [&](int kb) -> int {
-        const int p = kb * BK + Q * warp + static_cast<int>(lane % Q);
+        const int p = kidx(kb) * BK + Q * warp + static_cast<int>(lane % Q);
         return p < m.kpad ? neuron_at(m, a.idx, a.ld_idx, p) : a.f_local + (p - m.kpad);
       };
       // Neuron ids are prefetched 4 stages ahead (a register ring): an index load that
@@ -96,7 +99,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (kb + 4 < nk) r3 = row_of(kb + 4);
         // Contiguous K rows (identity index of dense blocks, compensator rows past kpad)
         // take the 2-D tile path: one 64-row box per column atom, issued by warp 0.
-        const bool contiguous = m.idx_row < 0 || kb * BK >= m.kpad;
+        const int kr = kidx(kb);  // K stage actually loaded (reversed tiles sweep downwards)
+        const bool contiguous = m.idx_row < 0 || kr * BK >= m.kpad;
         if (lane < Q) rows[lane] = cur;
         __syncwarp();
         if (lane == 0) {
@@ -109,10 +113,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&sm.bar->full[stage]);
           if (warp == 0) {
             if (!kSplit)
-              tma_load_2d(&tm_h, &sm.bar->full[stage], sm.a_stage(stage), kb * BK,
+              tma_load_2d(&tm_h, &sm.bar->full[stage], sm.a_stage(stage), kr * BK,
                           tl.b * kBlockTokens, pol_h);
             if (contiguous) {
-              const int r0 = m.idx_row < 0 ? kb * BK : a.f_local + (kb * BK - m.kpad);
+              const int r0 = m.idx_row < 0 ? kr * BK : a.f_local + (kr * BK - m.kpad);
 #pragma unroll
               for (int c = 0; c < kChunks; ++c)
                 tma_load_2d(&tm_wt, &sm.bar->full[stage], sm.b_stage(stage) + c * kLbo,
@@ -150,7 +154,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&sm.bar->emptyA[sa], pa ^ 1);
           mbar_arrive_expect_tx(&sm.bar->fullA[sa], kABytes);
-          tma_load_2d(&tm_h, &sm.bar->fullA[sa], sm.a_stage(sa), kb * BK, tl.b * kBlockTokens,
+          const int kr = tl.pad ? nk - 1 - kb : kb;
+          tma_load_2d(&tm_h, &sm.bar->fullA[sa], sm.a_stage(sa), kr * BK, tl.b * kBlockTokens,
                       pol_h);
           advance_n<kStagesA>(sa, pa);
         }

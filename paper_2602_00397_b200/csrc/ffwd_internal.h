@@ -28,7 +28,7 @@ struct Tile {
   int b;
   int n0;    // neuron position (gate/up), comp column (comp) or output column (down)
   int kind;  // 0 = gate/up, 1 = compensator hidden, 2 = down
-  int pad;
+  int pad;   // down tiles: 1 = walk the K stages from the top down (serpentine raster)
 };
 
 struct PlanCounts {

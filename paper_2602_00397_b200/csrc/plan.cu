@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
     const int sz = min(a.down_group, a.n_blk - o0);
     const int rel = slot - o0 * nt;
     const int j = rel / sz, o = o0 + rel % sz;
-    down[slot] = Tile{order_to_block(o, a), j * a.bn_down, 2, 0};
+    down[slot] = Tile{order_to_block(o, a), j * a.bn_down, 2, (a.serpentine && (g & 1)) ? 1 : 0};
   }
   if (tid == 0) {
     pc->n_up = total_up;
