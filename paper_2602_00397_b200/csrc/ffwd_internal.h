@@ -84,6 +84,7 @@ struct PlanArgs {
   int bn_down;                     // output columns per down tile
   int hcols_alloc;
   int serpentine;                  // odd up-projection raster groups sweep tiles downwards
+  int pair_up;                     // up tiles ordered in (i, i+1) pairs of one block
 };
 
 cudaError_t launch_plan(const PlanArgs& a, BlockMeta* meta, Tile* up_tiles, int up_cap,
@@ -114,6 +115,7 @@ struct GemmArgs {
 };
 
 cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s);
+bool up_proj_paired();  // the up projection runs as CTA pairs (tile table in pairs)
 cudaError_t launch_down_proj(const GemmArgs& a, cudaStream_t s);
 
 // tensor-map encoder (driver entry point resolved once through the runtime)

@@ -44,6 +44,14 @@ constexpr bool kSplit = false;
 constexpr int kStagesA = kStages;
 constexpr int kStagesB = kStages;
 #endif
+// CTA pairs (FFWD_PAIR_A, split rings only): the two CTAs of a cluster work on two
+// neuron tiles of the same token block at the same time and each loads half of the
+// shared A tile, multicast to both; both MMAs release every A slot in both CTAs.
+#ifdef FFWD_PAIR_A
+constexpr bool kPairA = true;
+#else
+constexpr bool kPairA = false;
+#endif
 #ifndef FFWD_PRODUCER_WARPS
 #define FFWD_PRODUCER_WARPS 8
 #endif
@@ -101,7 +109,7 @@ __device__ __forceinline__ void prologue(Smem<kBBytes>& sm, int warp) {
     }
     for (int i = 0; i < kStagesA; ++i) {
       mbar_init(&sm.bar->fullA[i], 1);
-      mbar_init(&sm.bar->emptyA[i], 1);
+      mbar_init(&sm.bar->emptyA[i], kPairA ? 2 : 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&sm.bar->tfull[i], 1);
@@ -112,6 +120,7 @@ __device__ __forceinline__ void prologue(Smem<kBBytes>& sm, int warp) {
   if (warp == kMmaWarp) tmem_alloc<kTmemCols>(&sm.bar->tmem_base);
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPairA) cluster_sync_all();  // peers' barriers initialised before any multicast
   tc_fence_after();
 }
 
@@ -119,6 +128,7 @@ template <int kBBytes>
 __device__ __forceinline__ void teardown(Smem<kBBytes>& sm, int warp) {
   tc_fence_before();
   __syncthreads();
+  if constexpr (kPairA) cluster_sync_all();  // no CTA leaves while its peer may still signal it
   tc_fence_after();
   if (warp == kMmaWarp) tmem_dealloc<kTmemCols>(sm.bar->tmem_base);
 }
@@ -187,7 +197,10 @@ __device__ __forceinline__ void mma_tile_split(Smem<kBBytes>& sm, uint32_t tmem_
                 (kb | kk) != 0 ? 1u : 0u);
     }
     umma_commit(&sm.bar->empty[sb]);
-    umma_commit(&sm.bar->emptyA[sa]);
+    if constexpr (kPairA)
+      umma_commit_mc(&sm.bar->emptyA[sa], 0x3);  // both CTAs' A slot sa is free of this MMA
+    else
+      umma_commit(&sm.bar->emptyA[sa]);
     advance_n<kStagesB>(sb, pb);
     advance_n<kStagesA>(sa, pa);
   }

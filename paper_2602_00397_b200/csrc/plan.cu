@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
     const int o1 = min(g < g_dense ? n_dense : a.n_blk, o0 + a.up_group);
     int mx = 0;
     for (int o = o0; o < o1; ++o) mx = max(mx, static_cast<int>(s_nup[o]));
+    if (a.pair_up) mx = rup(mx, 2);  // paired up-projection: whole (i, i+1) tile pairs
     s_gbase[g + 1] = mx * (o1 - o0);
   }
   __syncthreads();
@@ -100,11 +101,24 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
     const int sz = o1 - o0;
     const int rel = slot - s_gbase[lo];
     const int mx = (s_gbase[lo + 1] - s_gbase[lo]) / sz;  // tiles per block in this group
-    int i = rel / sz;
-    const int o = o0 + rel % sz;
-    // serpentine: odd groups sweep the neuron tiles downwards, so the weight rows the
-    // previous group touched last are still in L2 when the next group starts
-    if (a.serpentine && (lo & 1)) i = mx - 1 - i;
+    int i, o;
+    if (a.pair_up) {
+      // consecutive slots (2m, 2m + 1) = neuron tiles (2 i2, 2 i2 + 1) of ONE block: the
+      // CTA pair running them shares the block's X tile by TMA multicast.  An odd tile
+      // count repeats the block's last tile in the second slot (identical H writes).
+      const int pi = rel >> 1, h = rel & 1;
+      int i2 = pi / sz;
+      o = o0 + pi % sz;
+      if (a.serpentine && (lo & 1)) i2 = mx / 2 - 1 - i2;
+      i = 2 * i2 + h;
+      if (h == 1 && i == s_nup[o]) i -= 1;
+    } else {
+      i = rel / sz;
+      o = o0 + rel % sz;
+      // serpentine: odd groups sweep the neuron tiles downwards, so the weight rows the
+      // previous group touched last are still in L2 when the next group starts
+      if (a.serpentine && (lo & 1)) i = mx - 1 - i;
+    }
     Tile t{-1, 0, 0, 0};
     if (i < s_ngu[o]) {
       t = Tile{order_to_block(o, a), i * 128, 0, 0};

@@ -15,11 +15,15 @@
 #ifndef FFWD_PRODUCER_WARPS
 #define FFWD_PRODUCER_WARPS 16
 #endif
-// The gathers' fill latency bounds this kernel (no-B timing experiment: 1.78 -> 1.38
-// ms/layer; halving the gathers: -5%), so B gets a 5-deep ring and A a 4-deep one
-// loaded by its own warp (smem 4 x 16 + 5 x 32 KiB).
+// B (the gathers) gets a 5-deep ring and A a 4-deep one loaded by its own warp (smem
+// 4 x 16 + 5 x 32 KiB); the two CTAs of a cluster run neuron tiles (i, i+1) of the same
+// token block and each loads half of the block's X tile, multicast to both.
 #ifndef FFWD_UP_UNSPLIT
 #define FFWD_SPLIT_RING
+// CTA pairs sharing X by TMA multicast (L2->SM bytes -11%, in-stack K2 -1.5..2.7%).
+#ifndef FFWD_UP_NOPAIR
+#define FFWD_PAIR_A
+#endif
 #ifndef FFWD_STAGES_A
 #define FFWD_STAGES_A 4
 #endif
@@ -41,7 +45,8 @@ constexpr int kBBytes = UP_BN * BK * 2;  // 32 KiB per stage
 __global__ void __launch_bounds__(kThreads, 1)
     up_proj_kernel(const __grid_constant__ CUtensorMap tm_x,
                    const __grid_constant__ CUtensorMap tm_w,
-                   const __grid_constant__ CUtensorMap tm_wt, GemmArgs a) {
+                   const __grid_constant__ CUtensorMap tm_wt,
+                   const __grid_constant__ CUtensorMap tm_xh, GemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   Smem<kBBytes> sm(smem_raw);
   const int warp = threadIdx.x >> 5;
@@ -132,9 +137,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (tl.b < 0) continue;
         const int tok0 = a.meta[tl.b].tok0;
         for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(&sm.bar->emptyA[sa], pa ^ 1);
+          mbar_wait(&sm.bar->emptyA[sa], pa ^ 1);  // paired: both CTAs' MMAs released it
           mbar_arrive_expect_tx(&sm.bar->fullA[sa], kABytes);
-          tma_load_2d(&tm_x, &sm.bar->fullA[sa], sm.a_stage(sa), kb * BK, tok0, pol_x);
+          if constexpr (kPairA) {  // my 64-row half of X_b, multicast to both CTAs
+            const uint32_t cr = cluster_ctarank();
+            tma_load_2d_mc(&tm_xh, &sm.bar->fullA[sa], sm.a_stage(sa) + cr * (kABytes / 2),
+                           kb * BK, tok0 + static_cast<int>(cr) * (BM / 2), 0x3, pol_x);
+          } else {
+            tma_load_2d(&tm_x, &sm.bar->fullA[sa], sm.a_stage(sa), kb * BK, tok0, pol_x);
+          }
           advance_n<kStagesA>(sa, pa);
         }
       }
@@ -227,9 +238,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
+bool up_proj_paired() { return kPairA; }
+
 cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s) {
-  CUtensorMap tx, tw, twt;
+  CUtensorMap tx, tw, twt, txh;
   if (encode_tmap_2d_bf16(&tx, a.x, a.d, a.T, BK, BM) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  if (encode_tmap_2d_bf16(&txh, a.x, a.d, a.T, BK, BM / 2) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   if (encode_tmap_2d_bf16(&tw, a.wgu_t, a.d, a.wgu_rows, BK, 1) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
@@ -243,8 +258,25 @@ cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int grid = a.num_sms < a.up_cap ? a.num_sms : a.up_cap;
-  up_proj_kernel<<<grid, kThreads, smem, s>>>(tx, tw, twt, a);
+  int grid = a.num_sms < a.up_cap ? a.num_sms : a.up_cap;
+  if constexpr (kPairA) {
+    grid &= ~1;  // whole CTA pairs; the plan pads the tile table to pairs
+    if (grid < 2) grid = 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, up_proj_kernel, tx, tw, twt, txh, a);
+  }
+  up_proj_kernel<<<grid, kThreads, smem, s>>>(tx, tw, twt, txh, a);
   return cudaGetLastError();
 }
 
