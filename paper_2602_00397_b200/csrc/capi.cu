@@ -173,7 +173,7 @@ Ffn carve_ffn(Carve& c, int T, int d, int f_local, int rc_local, int kmax, int n
   const int tiles_dense = (f_local + 127) / 128;
   const int tiles_sparse = (kmax + 127) / 128 + (rc64 + 255) / 256;
   w.up_cap = n_blk * rup(tiles_dense > tiles_sparse ? tiles_dense : tiles_sparse, 2);
-  w.down_cap = n_blk * (d / bn_for(d));
+  w.down_cap = n_blk * rup(d / bn_for(d), 2);
   w.hcols = rup(rup(f_local, 64) > rup(kmax, 64) + rc64 ? rup(f_local, 64) : rup(kmax, 64) + rc64,
                 64);
   w.ld_local = ld_local;
@@ -223,6 +223,7 @@ int run_ffn(const void* x, int T, int d, const void* wgu_t, const void* wd, int 
   pa.hcols_alloc = w.hcols;
   pa.serpentine = g_serpentine;
   pa.pair_up = up_proj_paired() ? 1 : 0;
+  pa.pair_down = down_proj_paired() ? 1 : 0;
   {
     StageTimer tm(kPlan, s);
     FFWD_CUDA(launch_plan(pa, w.meta, w.up, w.up_cap, w.down, w.down_cap, w.pc, s), "plan");

@@ -14,7 +14,15 @@
 #ifndef FFWD_PRODUCER_WARPS
 #define FFWD_PRODUCER_WARPS 8
 #endif
-// Split rings as in K2 (A = H on its own loader warp, 4-deep; gathered B 5-deep).
+// Options (off by default): split rings as in K2 (A = H on its own loader warp, 4-deep;
+// gathered B 5-deep) and CTA pairs (FFWD_DOWN_PAIR: the two CTAs of a cluster run column
+// tiles (j, j+1) of one block and each loads half of its H tile, multicast to both).
+// ncu, 8B/16K: pairs cut K3's L2->SM bytes 6.8% but raise its DRAM reads from 1.64 to
+// 2.0-2.4 GB for every raster group size, and are within noise in the stack.
+#ifdef FFWD_DOWN_PAIR
+#define FFWD_DOWN_SPLIT
+#define FFWD_PAIR_A
+#endif
 #ifdef FFWD_DOWN_SPLIT
 #define FFWD_SPLIT_RING
 #ifndef FFWD_STAGES_A
@@ -48,7 +56,8 @@ template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     down_proj_kernel(const __grid_constant__ CUtensorMap tm_h,
                      const __grid_constant__ CUtensorMap tm_w,
-                     const __grid_constant__ CUtensorMap tm_wt, GemmArgs a) {
+                     const __grid_constant__ CUtensorMap tm_wt,
+                     const __grid_constant__ CUtensorMap tm_hh, GemmArgs a) {
   constexpr int kBBytes = BK * BN * 2;
   constexpr int kChunks = BN / 64;            // 64-column (128 B) atoms along N
   constexpr uint32_t kLbo = (BK / 8) * 1024;  // MN-direction atom stride
@@ -155,8 +164,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&sm.bar->emptyA[sa], pa ^ 1);
           mbar_arrive_expect_tx(&sm.bar->fullA[sa], kABytes);
           const int kr = tl.pad ? nk - 1 - kb : kb;
-          tma_load_2d(&tm_h, &sm.bar->fullA[sa], sm.a_stage(sa), kr * BK, tl.b * kBlockTokens,
-                      pol_h);
+          if constexpr (kPairA) {  // my 64-row half of H_b, multicast to both CTAs
+            const uint32_t cr = cluster_ctarank();
+            tma_load_2d_mc(&tm_hh, &sm.bar->fullA[sa], sm.a_stage(sa) + cr * (kABytes / 2),
+                           kr * BK, tl.b * kBlockTokens + static_cast<int>(cr) * (BM / 2), 0x3,
+                           pol_h);
+          } else {
+            tma_load_2d(&tm_h, &sm.bar->fullA[sa], sm.a_stage(sa), kr * BK, tl.b * kBlockTokens,
+                        pol_h);
+          }
           advance_n<kStagesA>(sa, pa);
         }
       }
@@ -203,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t v[16];
         tmem_ld16(tb + c, v);
         tmem_ld_wait();
-        if (live) {
+        if (live && tl.kind != 3) {  // kind 3: pair shadow, no stores
           float o[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) o[j] = __uint_as_float(v[j]);
@@ -249,8 +265,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int BN>
 cudaError_t launch_bn(const GemmArgs& a, cudaStream_t s) {
-  CUtensorMap th, tw, twt;
+  CUtensorMap th, tw, twt, thh;
   if (encode_tmap_2d_bf16(&th, a.h, a.hcols, static_cast<uint64_t>(a.n_blk) * BM, BK, BM) !=
+      CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  if (encode_tmap_2d_bf16(&thh, a.h, a.hcols, static_cast<uint64_t>(a.n_blk) * BM, BK, BM / 2) !=
       CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   if (encode_tmap_2d_bf16(&tw, a.wd, a.d, a.wd_rows, 64, 1) != CUDA_SUCCESS)
@@ -265,12 +284,31 @@ cudaError_t launch_bn(const GemmArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int grid = a.num_sms < a.down_cap ? a.num_sms : a.down_cap;
-  down_proj_kernel<BN><<<grid, kThreads, smem, s>>>(th, tw, twt, a);
+  int grid = a.num_sms < a.down_cap ? a.num_sms : a.down_cap;
+  if constexpr (kPairA) {
+    grid &= ~1;  // whole CTA pairs; the plan pads the tile table to pairs
+    if (grid < 2) grid = 2;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, down_proj_kernel<BN>, th, tw, twt, thh, a);
+  }
+  down_proj_kernel<BN><<<grid, kThreads, smem, s>>>(th, tw, twt, thh, a);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+bool down_proj_paired() { return kPairA; }
 
 cudaError_t launch_down_proj(const GemmArgs& a, cudaStream_t s) {
   switch (a.bn_down) {

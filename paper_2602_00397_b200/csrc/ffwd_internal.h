@@ -27,7 +27,7 @@ struct BlockMeta {
 struct Tile {
   int b;
   int n0;    // neuron position (gate/up), comp column (comp) or output column (down)
-  int kind;  // 0 = gate/up, 1 = compensator hidden, 2 = down
+  int kind;  // 0 = gate/up, 1 = compensator hidden, 2 = down, 3 = down shadow (no stores)
   int pad;   // down tiles: 1 = walk the K stages from the top down (serpentine raster)
 };
 
@@ -85,6 +85,7 @@ struct PlanArgs {
   int hcols_alloc;
   int serpentine;                  // odd up-projection raster groups sweep tiles downwards
   int pair_up;                     // up tiles ordered in (i, i+1) pairs of one block
+  int pair_down;                   // down tiles ordered in (j, j+1) column pairs of one block
 };
 
 cudaError_t launch_plan(const PlanArgs& a, BlockMeta* meta, Tile* up_tiles, int up_cap,
@@ -115,7 +116,8 @@ struct GemmArgs {
 };
 
 cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s);
-bool up_proj_paired();  // the up projection runs as CTA pairs (tile table in pairs)
+bool up_proj_paired();    // the up projection runs as CTA pairs (tile table in pairs)
+bool down_proj_paired();  // the down projection runs as CTA pairs
 cudaError_t launch_down_proj(const GemmArgs& a, cudaStream_t s);
 
 // tensor-map encoder (driver entry point resolved once through the runtime)

@@ -128,16 +128,33 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
     up[slot] = t;
   }
 
-  // down projection: groups of down_group blocks (raster order), column-tile major
+  // down projection: groups of down_group blocks (raster order), column-tile major.
+  // Paired (pair_down): slots (2m, 2m + 1) = column tiles (2 j2, 2 j2 + 1) of one block,
+  // sharing its H tile by multicast; an odd column count pads the pair with a shadow
+  // tile (kind 3: same tile, epilogue stores skipped -- the residual add is in place).
   const int nt = a.d / a.bn_down;
-  const int total_down = min(a.n_blk * nt, down_cap);
+  const int ntp = a.pair_down ? rup(nt, 2) : nt;
+  const int total_down = min(a.n_blk * ntp, down_cap);
   for (int slot = tid; slot < total_down; slot += kPlanThreads) {
-    const int g = slot / (a.down_group * nt);
+    const int g = slot / (a.down_group * ntp);
     const int o0 = g * a.down_group;
     const int sz = min(a.down_group, a.n_blk - o0);
-    const int rel = slot - o0 * nt;
-    const int j = rel / sz, o = o0 + rel % sz;
-    down[slot] = Tile{order_to_block(o, a), j * a.bn_down, 2, (a.serpentine && (g & 1)) ? 1 : 0};
+    const int rel = slot - o0 * ntp;
+    int j, o, kind = 2;
+    if (a.pair_down) {
+      const int pi = rel >> 1, h = rel & 1;
+      j = 2 * (pi / sz) + h;
+      o = o0 + pi % sz;
+      if (j == nt) {
+        j = nt - 1;
+        kind = 3;
+      }
+    } else {
+      j = rel / sz;
+      o = o0 + rel % sz;
+    }
+    down[slot] = Tile{order_to_block(o, a), j * a.bn_down, kind,
+                      (a.serpentine && (g & 1)) ? 1 : 0};
   }
   if (tid == 0) {
     pc->n_up = total_up;
