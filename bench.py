@@ -73,6 +73,16 @@ def load_peaks() -> dict:
     return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback"}
 
 
+# One process per GPU over NCCL.  FFWD_BENCH_BACKEND=gloo is a functional emulation for
+# tests: every rank shares GPU 0 (time-sliced; numbers meaningless), which exercises the
+# tensor-parallel path with the fused peer-memory completion (no NCCL data path) on one GPU.
+BACKEND = os.environ.get("FFWD_BENCH_BACKEND", "nccl")
+
+
+def local_device() -> int:
+    return 0 if BACKEND == "gloo" else int(os.environ.get("LOCAL_RANK", 0))
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
@@ -332,7 +342,7 @@ def run_gpu(args, rank: int, world: int) -> None:
     import paper_2602_00397_b200 as ff
     from paper_2602_00397_b200 import layer as fl
     from paper_2602_00397_b200.norm import rmsnorm
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", local_device())
     torch.cuda.set_device(dev)
     if args.raster:
         fl.set_raster(*(int(v) for v in args.raster.split(",")))
@@ -398,8 +408,8 @@ def run_gpu(args, rank: int, world: int) -> None:
         torch.cuda.synchronize(dev)
         barrier()
         ms = e0.elapsed_time(e1) / steps
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
+        if world > 1:  # max over ranks (a CPU tensor under the gloo emulation backend)
+            t = torch.tensor([ms], device="cpu" if BACKEND == "gloo" else dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ms = float(t.item())
         return ms
@@ -555,8 +565,8 @@ def main():
         run_reference(args, rank, world)
         return
     if world > 1:
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        torch.distributed.init_process_group("nccl")
+        torch.cuda.set_device(local_device())
+        torch.distributed.init_process_group(BACKEND)
     try:
         run_gpu(args, rank, world)
     finally:

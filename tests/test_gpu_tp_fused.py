@@ -141,3 +141,30 @@ def test_peer_buffers_across_processes(ff):
     results = sorted(q.get(timeout=5) for _ in range(2))
     assert all(p.exitcode == 0 for p in procs)
     assert results == [(0, True, True), (1, True, True)]
+
+
+def test_bench_tensor_parallel_fused_path_runs(ff):
+    """bench.py under torchrun, 2 ranks, --collective fused, emulated on the one GPU (gloo
+    for the host-side rendezvous, both ranks time-sliced on GPU 0): the TP sharding, the
+    CUDA IPC peer buffers and the fused completion run end to end and the JSON line is
+    well formed.  (Timings from this emulation are meaningless.)"""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, FFWD_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "2",
+           "--config", "1b", "--layers", "2", "--steps", "2", "--warmup", "3",
+           "--collective", "fused"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=400)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
+    d = json.loads(line)
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "tp2"
+    assert d["config"]["collective"] == "fused" and d["value"] > 0
