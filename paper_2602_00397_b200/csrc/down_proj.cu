@@ -11,9 +11,10 @@
 // f32 in TMEM.  Epilogue: optional residual add (engine.py:308) and optional
 // bf16 copy for the next layer's input, f32 Y stores.
 // 8 issuing warps (r1 A/B: 16 warps gave no gain here: 1.07 vs 1.09 ms/layer).
-#ifndef FFWD_PRODUCER_WARPS
-#define FFWD_PRODUCER_WARPS 8
+#ifndef FFWD_DOWN_PRODUCERS
+#define FFWD_DOWN_PRODUCERS 8
 #endif
+#define FFWD_PRODUCER_WARPS FFWD_DOWN_PRODUCERS
 // Options (off by default): split rings as in K2 (A = H on its own loader warp, 4-deep;
 // gathered B 5-deep) and CTA pairs (FFWD_DOWN_PAIR: the two CTAs of a cluster run column
 // tiles (j, j+1) of one block and each loads half of its H tile, multicast to both).

@@ -12,9 +12,10 @@
 // epilogue, written as bf16 into H (row stride hcols, block b at rows 128 b).
 // 16 issuing warps: gathers here are 128 B rows at 8 KiB stride, the up projection is
 // gather-rate bound (r1 A/B: 2.39 -> 2.21 ms/layer vs 8 warps).
-#ifndef FFWD_PRODUCER_WARPS
-#define FFWD_PRODUCER_WARPS 16
+#ifndef FFWD_UP_PRODUCERS
+#define FFWD_UP_PRODUCERS 16
 #endif
+#define FFWD_PRODUCER_WARPS FFWD_UP_PRODUCERS
 // B (the gathers) gets a 5-deep ring and A a 4-deep one loaded by its own warp (smem
 // 4 x 16 + 5 x 32 KiB); the two CTAs of a cluster run neuron tiles (i, i+1) of the same
 // token block and each loads half of the block's X tile, multicast to both.
