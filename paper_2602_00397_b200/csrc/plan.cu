@@ -1,4 +1,5 @@
-// Device-side tile planning for the up / down gather-GEMMs.
+// Device-side tile planning for the up / down gather-GEMMs (a few CTAs: each recomputes
+// the per-block prefix and writes a strided share of the tile slots).
 //
 // Reads the per-block neuron counts the top-k kernel produced (ragged under
 // tensor parallelism) and writes the block descriptors plus both persistent
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
     m.kpad = rup(m.kcount, 64);
     m.ktot = m.kpad + m.comp;
     m.n_gu = (m.kcount + 127) / 128;
-    meta[b] = m;
+    if (blockIdx.x == 0) meta[b] = m;
     s_ngu[o] = static_cast<short>(m.n_gu);
     s_nup[o] = static_cast<short>(m.n_gu + (m.comp + kUpBN - 1) / kUpBN);
     atomicMax(&s_hcols, m.ktot);
@@ -90,7 +91,8 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
   }
   __syncthreads();
   const int total_up = min(s_gbase[g_total], up_cap);
-  for (int slot = tid; slot < total_up; slot += kPlanThreads) {
+  for (int slot = blockIdx.x * kPlanThreads + tid; slot < total_up;
+       slot += gridDim.x * kPlanThreads) {
     int lo = 0, hi = g_total - 1;  // last group with base <= slot
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -135,7 +137,8 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
   const int nt = a.d / a.bn_down;
   const int ntp = a.pair_down ? rup(nt, 2) : nt;
   const int total_down = min(a.n_blk * ntp, down_cap);
-  for (int slot = tid; slot < total_down; slot += kPlanThreads) {
+  for (int slot = blockIdx.x * kPlanThreads + tid; slot < total_down;
+       slot += gridDim.x * kPlanThreads) {
     const int g = slot / (a.down_group * ntp);
     const int o0 = g * a.down_group;
     const int sz = min(a.down_group, a.n_blk - o0);
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
     down[slot] = Tile{order_to_block(o, a), j * a.bn_down, kind,
                       (a.serpentine && (g & 1)) ? 1 : 0};
   }
-  if (tid == 0) {
+  if (blockIdx.x == 0 && tid == 0) {
     pc->n_up = total_up;
     pc->n_down = total_down;
     pc->hcols = s_hcols;
@@ -168,7 +171,10 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
 cudaError_t launch_plan(const PlanArgs& a, BlockMeta* meta, Tile* up_tiles, int up_cap,
                         Tile* down_tiles, int down_cap, PlanCounts* counts, cudaStream_t s) {
   if (a.n_blk > kMaxBlocks) return cudaErrorInvalidValue;
-  plan_kernel<<<1, kPlanThreads, 0, s>>>(a, meta, up_tiles, up_cap, down_tiles, down_cap,
+  // every CTA rebuilds the per-block prefix (cheap) and writes its share of the slots
+  const int ctas = (up_cap + down_cap + 4 * kPlanThreads - 1) / (4 * kPlanThreads);
+  plan_kernel<<<ctas < 1 ? 1 : (ctas > 32 ? 32 : ctas), kPlanThreads, 0, s>>>(
+      a, meta, up_tiles, up_cap, down_tiles, down_cap,
                                          counts);
   return cudaGetLastError();
 }
