@@ -310,21 +310,24 @@ def measure_ttft(layers, cfg_name: str, dev, steps: int) -> dict:
                         final_norm=ones, head=w(d, VOCAB, dt=torch.float32),
                         dense_first_last=True, attn_dtype=torch.bfloat16, has_comp=True)
     tokens = np.random.default_rng(7).integers(0, VOCAB, T)
-    out = {}
+    out = {"predicted": [], "dense": []}
     for mode in ("predicted", "dense", "predicted", "dense"):  # warm-up (cuDNN plans, pools)
         prefill(model, tokens, mode=mode).last_logits.cpu()
-    for mode in ("predicted", "dense"):
-        torch.cuda.synchronize(dev)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(steps):
+    torch.cuda.synchronize(dev)
+    flops = {}
+    for _ in range(steps):  # alternate the modes so clock / power drift hits both alike
+        for mode in ("predicted", "dense"):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
             res = prefill(model, tokens, mode=mode)
             res.last_logits.cpu()
-        e1.record()
-        torch.cuda.synchronize(dev)
-        ms = e0.elapsed_time(e1) / steps
-        out[mode] = {"ms": ms, "flops": int(res.flops.total()),
-                     "effective_tflops": res.flops.total() / (ms * 1e-3) / 1e12}
+            e1.record()
+            torch.cuda.synchronize(dev)
+            out[mode].append(e0.elapsed_time(e1))
+            flops[mode] = int(res.flops.total())
+    out = {m: {"ms": statistics.mean(v), "flops": flops[m],
+               "effective_tflops": flops[m] / (statistics.mean(v) * 1e-3) / 1e12}
+           for m, v in out.items()}
     del model, dls
     torch.cuda.empty_cache()
     return {"unit": "ms", "T": T, "layers": L, "n_heads": cfg.n_heads, "vocab": VOCAB,
@@ -334,7 +337,7 @@ def measure_ttft(layers, cfg_name: str, dev, steps: int) -> dict:
             "dense_effective_tflops": out["dense"]["effective_tflops"],
             "attention": "torch SDPA (cuDNN/flash, bf16), QKV/O projections cuBLAS bf16",
             "timed": "host token ids -> host last-token logits, CUDA events, mean of "
-                     f"{steps} prefills after 2 warm-up prefills per mode"}
+                     f"{steps} prefills per mode (modes alternated) after 2 warm-ups each"}
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -524,7 +527,7 @@ def run_gpu(args, rank: int, world: int) -> None:
                         "dense_tflops_cublas": 6 * T * d * f / (cub * 1e-3) / 1e12}
     # ---- TTFT of the full prefill (rank 0, single GPU)
     if world == 1 and not args.skip_ttft:
-        out["ttft"] = measure_ttft(layers, args.config, dev, max(1, min(3, args.steps)))
+        out["ttft"] = measure_ttft(layers, args.config, dev, max(1, min(4, args.steps)))
     del layers
     torch.cuda.empty_cache()
 
