@@ -60,6 +60,9 @@ FFWD_API int ffwd_set_raster(int up_group, int down_group);
 /* Tuning knob: odd up-projection raster groups sweep their neuron tiles downwards (1,
  * default) so the previous group's last weight rows are still in L2. */
 FFWD_API int ffwd_set_serpentine(int on);
+/* Programmatic dependent launch of the hot-path kernels (1, default): each kernel's
+ * prologue overlaps its predecessor's tail; 0 = plain stream serialisation. */
+FFWD_API int ffwd_set_pdl(int on);
 
 /*
  * Predictor scores for blocks [blk_begin, blk_begin + blk_count) of x.

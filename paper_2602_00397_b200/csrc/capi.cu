@@ -24,6 +24,10 @@ namespace {
 thread_local std::string g_err;
 int g_up_group = 32;
 int g_serpentine = 1;
+#ifndef FFWD_PDL_DEFAULT
+#define FFWD_PDL_DEFAULT 1
+#endif
+int g_pdl = FFWD_PDL_DEFAULT;
 int g_down_group = 16;  // ncu sweep: K3 DRAM 3.0 GB -> 1.7 GB per layer vs 8 (profiles/r1_raster_sweep.txt)
 
 int fail(int code, const char* fmt, ...) {
@@ -274,6 +278,10 @@ int check_gemm_shapes(int d, int f_local) {
 
 }  // namespace
 
+namespace ffwd {
+bool pdl_enabled() { return g_pdl != 0; }
+}  // namespace ffwd
+
 extern "C" {
 
 int ffwd_abi_version(void) { return FFWD_ABI_VERSION; }
@@ -287,6 +295,11 @@ int ffwd_device_check(int device) {
   if (p.major != 10 || p.minor != 0)
     return fail(FFWD_ERR_UNSUPPORTED, "device %d is sm_%d%d; kernels are built for sm_100a",
                 device, p.major, p.minor);
+  return FFWD_OK;
+}
+
+int ffwd_set_pdl(int on) {
+  g_pdl = on != 0;
   return FFWD_OK;
 }
 

@@ -34,6 +34,7 @@
 #endif
 #endif
 #include "gemm_sm100.cuh"
+#include "launch.cuh"
 
 // L2 policies (A/B tuning knobs): 0 evict_normal, 1 evict_first, 2 evict_last.
 #ifndef FFWD_K3_H_POLICY
@@ -72,6 +73,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tm_wt);
   }
   prologue(sm, warp);
+  pdl_wait();  // the prologue overlapped the predecessor; H, tile tables are its output
+  pdl_trigger();
   const uint32_t tmem = sm.bar->tmem_base;
   const int n_tiles = a.counts->n_down;
 
@@ -289,22 +292,9 @@ cudaError_t launch_bn(const GemmArgs& a, cudaStream_t s) {
   if constexpr (kPairA) {
     grid &= ~1;  // whole CTA pairs; the plan pads the tile table to pairs
     if (grid < 2) grid = 2;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid, 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, down_proj_kernel<BN>, th, tw, twt, thh, a);
   }
-  down_proj_kernel<BN><<<grid, kThreads, smem, s>>>(th, tw, twt, thh, a);
-  return cudaGetLastError();
+  return launch_k(down_proj_kernel<BN>, dim3(grid), dim3(kThreads), smem, s, kPairA ? 2 : 1, th,
+                  tw, twt, thh, a);
 }
 
 }  // namespace

@@ -1,0 +1,53 @@
+// Kernel launch helper: programmatic dependent launch (PDL) on every hot-path kernel,
+// optionally as a thread-block cluster.
+//
+// A kernel launched with programmatic stream serialization may be scheduled while its
+// predecessor in the stream is still running; it calls pdl_wait() before touching
+// anything the predecessor produces (griddepcontrol.wait returns once the predecessor
+// grid has completed and its memory is visible) and pdl_trigger() to let its own
+// successor be scheduled early.  Every kernel waits before its first dependent access,
+// so ordering stays transitive along the stream; what overlaps is launch latency and
+// the prologues (barrier init, TMEM allocation, tensor-map prefetch, parameter loads).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <utility>
+
+namespace ffwd {
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+bool pdl_enabled();  // capi.cu: ffwd_set_pdl knob (default on)
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  unsigned n = 0;
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster_x > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = cluster_x;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+}  // namespace ffwd

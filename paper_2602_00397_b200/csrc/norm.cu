@@ -23,6 +23,7 @@
 #include <type_traits>
 
 #include "ffwd_internal.h"
+#include "launch.cuh"
 
 namespace ffwd {
 
@@ -61,6 +62,8 @@ __global__ void __launch_bounds__(kNormThreads, 2)
                    float* __restrict__ out_f32, const float* __restrict__ query, float sqrt_d,
                    float* __restrict__ logits, int logit_row0, int logit_row1) {
   __shared__ double red[kNormThreads / 32];
+  pdl_wait();
+  pdl_trigger();
   const int nv = d / 4;
   double gd[kMaxV][4], qd[kMaxV][4];
 #pragma unroll
@@ -230,9 +233,10 @@ cudaError_t launch_rmsnorm_t(float* x, const float* gain, int T, int d, double e
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = T < 2 * sms ? T : 2 * sms;
+  cudaError_t e = cudaSuccess;
 #define FFWD_NORM(V)                                                                       \
-  rmsnorm_kernel<V, kAdd><<<grid, kNormThreads, 0, s>>>(x, gain, T, d, eps, add, ob, out_f32, \
-                                                        query, sqrt_d, logits, r0, r1)
+  e = launch_k(rmsnorm_kernel<V, kAdd>, dim3(grid), dim3(kNormThreads), 0, s, 1, x, gain, T, d, \
+               eps, add, ob, out_f32, query, sqrt_d, logits, r0, r1)
   if (nv <= 1) FFWD_NORM(1);
   else if (nv <= 2) FFWD_NORM(2);
   else if (nv <= 4) FFWD_NORM(4);
@@ -240,7 +244,7 @@ cudaError_t launch_rmsnorm_t(float* x, const float* gain, int T, int d, double e
   else if (nv <= 16) FFWD_NORM(16);
   else return cudaErrorInvalidValue;
 #undef FFWD_NORM
-  return cudaGetLastError();
+  return e;
 }
 
 cudaError_t launch_rmsnorm(float* x, const float* gain, int T, int d, double eps,

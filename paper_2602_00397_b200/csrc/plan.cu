@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include "ffwd_internal.h"
+#include "launch.cuh"
 
 namespace ffwd {
 
@@ -41,6 +42,8 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
   __shared__ short s_ngu[kMaxBlocks];   // of which gate/up tiles
   __shared__ int s_gbase[kMaxBlocks + 1];
   __shared__ int s_hcols;
+  pdl_wait();
+  pdl_trigger();
   const int tid = threadIdx.x;
   const int rc64 = rup(a.rc_local, 64);
   if (tid == 0) s_hcols = 0;
@@ -173,10 +176,8 @@ cudaError_t launch_plan(const PlanArgs& a, BlockMeta* meta, Tile* up_tiles, int 
   if (a.n_blk > kMaxBlocks) return cudaErrorInvalidValue;
   // every CTA rebuilds the per-block prefix (cheap) and writes its share of the slots
   const int ctas = (up_cap + down_cap + 4 * kPlanThreads - 1) / (4 * kPlanThreads);
-  plan_kernel<<<ctas < 1 ? 1 : (ctas > 32 ? 32 : ctas), kPlanThreads, 0, s>>>(
-      a, meta, up_tiles, up_cap, down_tiles, down_cap,
-                                         counts);
-  return cudaGetLastError();
+  return launch_k(plan_kernel, dim3(ctas < 1 ? 1 : (ctas > 32 ? 32 : ctas)), dim3(kPlanThreads), 0,
+                  s, 1, a, meta, up_tiles, up_cap, down_tiles, down_cap, counts);
 }
 
 }  // namespace ffwd

@@ -23,6 +23,7 @@
 #include <type_traits>
 
 #include "ffwd_internal.h"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 namespace ffwd {
@@ -86,6 +87,8 @@ template <bool kF32>
 __global__ void __launch_bounds__(kLogitThreads)
     logits_kernel(const void* __restrict__ x, int d, int tok0, int ntok,
                   const float* __restrict__ query, float sqrt_d, float* __restrict__ logits) {
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int t = blockIdx.x * kLogitWarps + warp;
   if (t >= ntok) return;
@@ -136,6 +139,8 @@ __global__ void __launch_bounds__(kPoolThreads, 2)
   __shared__ double probd[kBlockTokens];
   __shared__ double wred[2][4];
   __shared__ double red[kPoolQuarters][kPoolCols];
+  pdl_wait();
+  pdl_trigger();
   const int rel = blk_count - 1 - static_cast<int>(blockIdx.y);
   const int tok0 = (blk_begin + rel) * kBlockTokens;
   const int n = min(kBlockTokens, T - tok0);
@@ -232,6 +237,8 @@ __global__ void __launch_bounds__(GTHREADS)
   constexpr int NJ = BN / 8;
   __shared__ __align__(16) float As[2][GBM * AP];
   __shared__ __align__(16) float Bs[2][GBK * BP];
+  pdl_wait();
+  pdl_trigger();
   const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * BN;
   const int k_lo = blockIdx.z * kper, k_hi = min(K, k_lo + kper);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -320,6 +327,8 @@ __global__ void __launch_bounds__(GTHREADS)
 
 __global__ void gemm_reduce_kernel(const double* __restrict__ partial, float* __restrict__ C,
                                    int MN, int splits, int relu) {
+  pdl_wait();
+  pdl_trigger();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= MN) return;
   double s = 0.0;
@@ -353,13 +362,21 @@ cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begi
   // RMSNorm; the first pass is then skipped.
   const float* lg = logits_in ? logits_in + tok0 : logits;
   if (x_is_f32) {
-    if (!logits_in)
-      logits_kernel<true><<<g1, kLogitThreads, 0, s>>>(x, d, tok0, ntok, query, sqrt_d, logits);
-    pooled_kernel<true><<<g2, kPoolThreads, 0, s>>>(x, T, d, blk_begin, blk_count, lg, pooled);
+    if (!logits_in) {
+      cudaError_t e = launch_k(logits_kernel<true>, g1, dim3(kLogitThreads), 0, s, 1, x, d, tok0,
+                               ntok, query, sqrt_d, logits);
+      if (e != cudaSuccess) return e;
+    }
+    return launch_k(pooled_kernel<true>, g2, dim3(kPoolThreads), 0, s, 1, x, T, d, blk_begin,
+                    blk_count, lg, pooled);
   } else {
-    if (!logits_in)
-      logits_kernel<false><<<g1, kLogitThreads, 0, s>>>(x, d, tok0, ntok, query, sqrt_d, logits);
-    pooled_kernel<false><<<g2, kPoolThreads, 0, s>>>(x, T, d, blk_begin, blk_count, lg, pooled);
+    if (!logits_in) {
+      cudaError_t e = launch_k(logits_kernel<false>, g1, dim3(kLogitThreads), 0, s, 1, x, d, tok0,
+                               ntok, query, sqrt_d, logits);
+      if (e != cudaSuccess) return e;
+    }
+    return launch_k(pooled_kernel<false>, g2, dim3(kPoolThreads), 0, s, 1, x, T, d, blk_begin,
+                    blk_count, lg, pooled);
   }
   return cudaGetLastError();
 }
@@ -379,15 +396,19 @@ cudaError_t launch_gemm_f64acc(const float* A, const float* B, float* C, int M, 
   // warps per SM keep the DMMA pipe busy.
   if (z == 1 && N >= 16 * 4 * 148) {
     const dim3 g16((N + 15) / 16, (M + GBM - 1) / GBM, 1);
-    gemm_f64_kernel<16><<<g16, GTHREADS, 0, s>>>(A, B, C, nullptr, M, K, N, kper, relu ? 1 : 0);
-    return cudaGetLastError();
+    return launch_k(gemm_f64_kernel<16>, g16, dim3(GTHREADS), 0, s, 1, A, B, C,
+                    static_cast<double*>(nullptr), M, K, N, kper, relu ? 1 : 0);
   }
   const dim3 grid((N + kGemmBN - 1) / kGemmBN, (M + GBM - 1) / GBM, z);
-  gemm_f64_kernel<kGemmBN><<<grid, GTHREADS, 0, s>>>(A, B, C, z > 1 ? partial : nullptr, M, K, N,
-                                                     kper, relu ? 1 : 0);
+  cudaError_t e = launch_k(gemm_f64_kernel<kGemmBN>, grid, dim3(GTHREADS), 0, s, 1, A, B, C,
+                           z > 1 ? partial : static_cast<double*>(nullptr), M, K, N, kper,
+                           relu ? 1 : 0);
+  if (e != cudaSuccess) return e;
   if (z > 1) {
     const int mn = M * N;
-    gemm_reduce_kernel<<<(mn + 255) / 256, 256, 0, s>>>(partial, C, mn, z, relu ? 1 : 0);
+    e = launch_k(gemm_reduce_kernel, dim3((mn + 255) / 256), dim3(256), 0, s, 1,
+                 static_cast<const double*>(partial), C, mn, z, relu ? 1 : 0);
+    if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
 }

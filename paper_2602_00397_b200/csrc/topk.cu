@@ -15,6 +15,7 @@
 #include <cstdint>
 
 #include "ffwd_internal.h"
+#include "launch.cuh"
 
 namespace ffwd {
 
@@ -79,6 +80,8 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
   __shared__ int s_total;
   __shared__ uint32_t s_prefix;
   __shared__ int s_remaining;
+  pdl_wait();
+  pdl_trigger();
   const float* s = scores + static_cast<size_t>(blockIdx.x) * f;
   const int tid = threadIdx.x;
   auto key_at = [&](int i) -> uint32_t {
@@ -209,13 +212,11 @@ cudaError_t launch_topk(const float* scores, int n_rows, int f, int k, int tp_ra
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    topk_kernel<true><<<n_rows, kTopkThreads, smem, s>>>(scores, f, k, tp_rank, tp_size,
-                                                         idx_global, ld_global, idx_local,
-                                                         ld_local, counts);
+    return launch_k(topk_kernel<true>, dim3(n_rows), dim3(kTopkThreads), smem, s, 1, scores, f,
+                    k, tp_rank, tp_size, idx_global, ld_global, idx_local, ld_local, counts);
   } else {
-    topk_kernel<false><<<n_rows, kTopkThreads, 0, s>>>(scores, f, k, tp_rank, tp_size,
-                                                       idx_global, ld_global, idx_local,
-                                                       ld_local, counts);
+    return launch_k(topk_kernel<false>, dim3(n_rows), dim3(kTopkThreads), 0, s, 1, scores, f,
+                    k, tp_rank, tp_size, idx_global, ld_global, idx_local, ld_local, counts);
   }
   return cudaGetLastError();
 }

@@ -33,6 +33,7 @@
 #endif
 #endif
 #include "gemm_sm100.cuh"
+#include "launch.cuh"
 
 namespace ffwd {
 
@@ -58,6 +59,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tm_wt);
   }
   prologue(sm, warp);
+  pdl_wait();  // the prologue overlapped the predecessor; tile tables, X, idx are its output
+  pdl_trigger();
   const uint32_t tmem = sm.bar->tmem_base;
   const int n_tiles = a.counts->n_up;
   const int nk = a.d / BK;
@@ -263,22 +266,9 @@ cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s) {
   if constexpr (kPairA) {
     grid &= ~1;  // whole CTA pairs; the plan pads the tile table to pairs
     if (grid < 2) grid = 2;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid, 1, 1);
-    cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, up_proj_kernel, tx, tw, twt, txh, a);
   }
-  up_proj_kernel<<<grid, kThreads, smem, s>>>(tx, tw, twt, txh, a);
-  return cudaGetLastError();
+  return launch_k(up_proj_kernel, dim3(grid), dim3(kThreads), smem, s, kPairA ? 2 : 1, tx, tw, twt,
+                  txh, a);
 }
 
 }  // namespace ffwd
