@@ -24,6 +24,10 @@ namespace {
 thread_local std::string g_err;
 int g_up_group = 32;
 int g_serpentine = 1;
+#ifndef FFWD_BLOCKDEP_DEFAULT
+#define FFWD_BLOCKDEP_DEFAULT 1
+#endif
+int g_blockdep = FFWD_BLOCKDEP_DEFAULT;
 #ifndef FFWD_PDL_DEFAULT
 #define FFWD_PDL_DEFAULT 1
 #endif
@@ -165,6 +169,7 @@ struct Ffn {
   Tile* down;
   PlanCounts* pc;
   __nv_bfloat16* h;
+  int* blk_done;
   int up_cap, down_cap, hcols, ld_local;
 };
 
@@ -187,6 +192,7 @@ Ffn carve_ffn(Carve& c, int T, int d, int f_local, int rc_local, int kmax, int n
   w.up = c.take<Tile>(w.up_cap);
   w.down = c.take<Tile>(w.down_cap);
   w.pc = c.take<PlanCounts>(1);
+  w.blk_done = c.take<int>(n_blk);
   w.h = c.take<__nv_bfloat16>(static_cast<size_t>(n_blk) * kBlockTokens * w.hcols);
   return w;
 }
@@ -228,6 +234,7 @@ int run_ffn(const void* x, int T, int d, const void* wgu_t, const void* wd, int 
   pa.serpentine = g_serpentine;
   pa.pair_up = up_proj_paired() ? 1 : 0;
   pa.pair_down = down_proj_paired() ? 1 : 0;
+  pa.blk_done = (g_blockdep && !up_only) ? w.blk_done : nullptr;
   {
     StageTimer tm(kPlan, s);
     FFWD_CUDA(launch_plan(pa, w.meta, w.up, w.up_cap, w.down, w.down_cap, w.pc, s), "plan");
@@ -257,6 +264,7 @@ int run_ffn(const void* x, int T, int d, const void* wgu_t, const void* wd, int 
   ga.counts = w.pc;
   ga.num_sms = num_sms();
   ga.bn_down = bn_for(d);
+  ga.blk_done = pa.blk_done;
   {
     StageTimer tm(kUp, s);
     FFWD_CUDA(launch_up_proj(ga, s), "up_proj");

@@ -54,6 +54,18 @@ namespace {
 
 using namespace gemm;
 
+// Spin until all `n` up-projection tiles of a block have published their H (K2 epilogue
+// counters), then make the writes visible to this thread's TMA loads.
+__device__ __forceinline__ void wait_block_h(const int* done, int n) {
+  while (true) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
+    if (v >= n) break;
+    __nanosleep(200);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     down_proj_kernel(const __grid_constant__ CUtensorMap tm_h,
@@ -73,7 +85,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     tma_prefetch_desc(&tm_wt);
   }
   prologue(sm, warp);
-  pdl_wait();  // the prologue overlapped the predecessor; H, tile tables are its output
+  // The tile tables come from the plan, which K2 waited for before letting K3 launch.
+  // With per-block counters K3 waits only for the H of the block each tile reads (A
+  // loads below), so its first tiles overlap K2's tail; otherwise wait for all of K2.
+  if (!a.blk_done) pdl_wait();
   pdl_trigger();
   const uint32_t tmem = sm.bar->tmem_base;
   const int n_tiles = a.counts->n_down;
@@ -125,6 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           else
             mbar_arrive(&sm.bar->full[stage]);
           if (warp == 0) {
+            if (kb == 0 && a.blk_done) wait_block_h(a.blk_done + tl.b, m.n_up);
             if (!kSplit)
               tma_load_2d(&tm_h, &sm.bar->full[stage], sm.a_stage(stage), kr * BK,
                           tl.b * kBlockTokens, pol_h);
@@ -164,6 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const Tile tl = a.down_tiles[t];
         if (tl.b < 0) continue;
         const int nk = a.meta[tl.b].ktot / BK;
+        if (a.blk_done) wait_block_h(a.blk_done + tl.b, a.meta[tl.b].n_up);
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(&sm.bar->emptyA[sa], pa ^ 1);
           mbar_arrive_expect_tx(&sm.bar->fullA[sa], kABytes);

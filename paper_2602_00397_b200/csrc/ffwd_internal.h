@@ -21,6 +21,7 @@ struct BlockMeta {
   int idx_row;   // row of the index buffer, -1 = identity (dense block)
   int ktot;      // kpad + comp : K extent of the down projection
   int n_gu;      // gate/up tiles (128 neurons each) for the up projection
+  int n_up;      // up-projection slots of the block (incl. a pair's repeated tile)
 };
 
 // Tile table entry: block id + packed (kind, offset).  b < 0 = empty slot.
@@ -86,6 +87,7 @@ struct PlanArgs {
   int serpentine;                  // odd up-projection raster groups sweep tiles downwards
   int pair_up;                     // up tiles ordered in (i, i+1) pairs of one block
   int pair_down;                   // down tiles ordered in (j, j+1) column pairs of one block
+  int* blk_done;                   // nullable: per-block up-tile counters, zeroed here
 };
 
 cudaError_t launch_plan(const PlanArgs& a, BlockMeta* meta, Tile* up_tiles, int up_cap,
@@ -113,6 +115,7 @@ struct GemmArgs {
   const PlanCounts* counts;
   int num_sms;
   int bn_down;
+  int* blk_done;  // nullable: block-granular K2 -> K3 dependency (per-block done tiles)
 };
 
 cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s);

@@ -67,9 +67,14 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
     m.kpad = rup(m.kcount, 64);
     m.ktot = m.kpad + m.comp;
     m.n_gu = (m.kcount + 127) / 128;
-    if (blockIdx.x == 0) meta[b] = m;
+    const int nup = m.n_gu + (m.comp + kUpBN - 1) / kUpBN;
+    m.n_up = a.pair_up ? rup(nup, 2) : nup;
+    if (blockIdx.x == 0) {
+      meta[b] = m;
+      if (a.blk_done) a.blk_done[b] = 0;
+    }
     s_ngu[o] = static_cast<short>(m.n_gu);
-    s_nup[o] = static_cast<short>(m.n_gu + (m.comp + kUpBN - 1) / kUpBN);
+    s_nup[o] = static_cast<short>(nup);
     atomicMax(&s_hcols, m.ktot);
   }
   __syncthreads();

@@ -231,6 +231,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
         }
       }
+      if (a.blk_done) {  // publish "one more H tile of block b is written" (K3 waits on it)
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (row == 0) atomicAdd(a.blk_done + tl.b, 1);
+      }
       tc_fence_before();
       mbar_arrive(&sm.bar->tempty[acc]);
       acc ^= 1;
