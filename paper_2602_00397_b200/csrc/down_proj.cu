@@ -55,13 +55,15 @@ namespace {
 using namespace gemm;
 
 // Spin until all `n` up-projection tiles of a block have published their H (K2 epilogue
-// counters), then make the writes visible to this thread's TMA loads.
+// counters), then make the writes visible to this thread's TMA loads.  Bounded: traps
+// after ~10 s rather than hanging the GPU.
 __device__ __forceinline__ void wait_block_h(const int* done, int n) {
-  while (true) {
+  for (long long spins = 0;; ++spins) {
     int v;
     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(done) : "memory");
     if (v >= n) break;
     __nanosleep(200);
+    if (spins > (1ll << 26)) __trap();  // K2 never published this block: fail, do not hang
   }
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
