@@ -271,3 +271,37 @@ def test_full_size_properties(ff, shape):
             want = orc.sparse_ffn_forward(xb, lw["w_gate"], lw["w_up"], lw["w_down"], idx[j - 1])
             want = want + orc.compensator_forward(comp["w1"], comp["w2"], xb)
         assert_close(y[j * 128:(j + 1) * 128], want, f"{name} block {j}")
+
+
+@pytest.mark.parametrize("d,f,T,k,dfl", [
+    (192, 520, 1, 17, True),      # one token, one (dense) block
+    (192, 520, 129, 259, True),   # second block holds one token; both dense
+    (192, 520, 300, 1, False),    # k = 1; 64-column down tiles (d % 128 != 0)
+    (192, 520, 300, 519, False),  # k = f - 1; odd up-tile counts (CTA-pair repeats)
+    (320, 1000, 400, 333, True),  # odd column-tile count in K3, ragged compensator
+    (256, 768, 640, 768, True),   # k == f: full-K shortcut, every block dense
+])
+def test_layer_edge_shapes_vs_oracle(ff, d, f, T, k, dfl):
+    """Edge shapes of the reference's own tests (short / single-token blocks, k = 1,
+    k = f - 1, k = f) and of this build's tiling (64/128-column down tiles, odd tile
+    counts under CTA pairs, ragged compensator): indices bit-exact, outputs in tolerance."""
+    rng = np.random.default_rng(d * 7 + T)
+    lw = orc.random_layer(rng, d, f, 0.02)
+    for key in ("w_gate", "w_up", "w_down"):
+        lw[key] = orc.bf16_round(lw[key])
+    pred = orc.init_predictor(np.random.default_rng([d, T]), d, f)
+    comp = {k_: orc.bf16_round(v) for k_, v in
+            orc.init_compensator(np.random.default_rng([d, T, 1]), d).items()}
+    x = orc.bf16_round(rng.standard_normal((T, d)).astype(np.float32))
+    packed = ff.pack_layer(lw["w_gate"], lw["w_up"], lw["w_down"], ff.CompensatorParams(**comp),
+                           device="cuda")
+    dp = dev_pred(ff, pred)
+    y, idx = ff.sparse_ffn_layer(torch.from_numpy(x).to("cuda", torch.bfloat16), packed, dp, k,
+                                 dense_first_last=dfl, return_indices=True)
+    torch.cuda.synchronize()
+    want, masks, _ = orc.ffn_layer_blockwise(x, lw, pred, comp, k, dfl, keep_masks=True)
+    if masks:
+        got = idx.cpu().numpy()
+        for row, j in enumerate(sorted(masks)):
+            np.testing.assert_array_equal(got[row], masks[j])
+    assert_close(y.cpu().numpy(), want, f"d{d} f{f} T{T} k{k}")
