@@ -24,6 +24,14 @@
 
 #include "ffwd_internal.h"
 #include "launch.cuh"
+
+// pooled_kernel tuning: tokens in flight per lane (bf16) and the CTAs-per-SM register bound
+#ifndef FFWD_POOL_BATCH
+#define FFWD_POOL_BATCH 8
+#endif
+#ifndef FFWD_POOL_MINB
+#define FFWD_POOL_MINB 3
+#endif
 #include "sm100.cuh"
 
 namespace ffwd {
@@ -133,7 +141,7 @@ __global__ void __launch_bounds__(kLogitThreads)
 // half h = w & 1 of the CTA's 512) for the 32 tokens of quarter w >> 1, with 16 loads
 // of 16 B in flight per lane; the four quarter partials are added in order.
 template <bool kF32>
-__global__ void __launch_bounds__(kPoolThreads, 2)
+__global__ void __launch_bounds__(kPoolThreads, FFWD_POOL_MINB)
     pooled_kernel(const void* __restrict__ x, int T, int d, int blk_begin, int blk_count,
                   const float* __restrict__ logits, float* __restrict__ pooled) {
   __shared__ double probd[kBlockTokens];
@@ -173,7 +181,7 @@ __global__ void __launch_bounds__(kPoolThreads, 2)
   for (int i = 0; i < 8; ++i) acc[i] = 0.0;
   if (c < d) {
     constexpr int kPer = kBlockTokens / kPoolQuarters;  // 32 tokens per warp
-    constexpr int kBatch = kF32 ? 8 : 16;               // tokens in flight per lane
+    constexpr int kBatch = kF32 ? FFWD_POOL_BATCH / 2 : FFWD_POOL_BATCH;  // tokens in flight
 #pragma unroll 1
     for (int t0 = quarter * kPer; t0 < quarter * kPer + kPer; t0 += kBatch) {
       Raw8<kF32> xr[kBatch];
