@@ -347,12 +347,22 @@ __global__ void gemm_reduce_kernel(const double* __restrict__ partial, float* __
   C[i] = v;
 }
 
-constexpr int kGemmBN = 32;
+// Split-K GEMMs (the W1 layer: few output tiles, long K) use kSplitBN-column tiles and at
+// most kMaxSplits K splits.
+#ifndef FFWD_SPLIT_BN
+#define FFWD_SPLIT_BN 32
+#endif
+#ifndef FFWD_MAX_SPLITS
+#define FFWD_MAX_SPLITS 32
+#endif
+constexpr int kGemmBN = FFWD_SPLIT_BN;
+constexpr int kMaxSplits = FFWD_MAX_SPLITS;
 
 int gemm_splits(int M, int K, int N) {
   const int tiles = ((N + kGemmBN - 1) / kGemmBN) * ((M + GBM - 1) / GBM);
   int splits = 1;
-  while (tiles * splits < 2 * 148 && K / (2 * splits) >= 2 * GBK && splits < 32) splits *= 2;
+  while (tiles * splits < 2 * 148 && K / (2 * splits) >= 2 * GBK && splits < kMaxSplits)
+    splits *= 2;
   return splits;
 }
 
