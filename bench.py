@@ -12,16 +12,21 @@ predictor and compensator) the FFN branch of engine.py:264-308 over all 128
 blocks -- the FFN-input RMSNorm of the f32 residual stream (fused with the
 predictor's per-token logits), predictor -> top-k -> sparse SwiGLU FFN +
 compensator -> residual add.  The norm keeps the stack numerically sane (an
-FFN-only stack without it overflows to inf by layer 6).  `value` = device time per step / 32 (ms per layer),
-inputs resident in HBM; `e2e` = the same stack through the public API with the
+FFN-only stack without it overflows to inf by layer 6).  `value` = device time
+per step / 32 (ms per layer), inputs resident in HBM, uninstrumented (the
+per-kernel breakdown comes from a second, event-timed run); `e2e` = the same stack through the public API with the
 prompt's hidden states copied from pinned host memory and the result copied
 back inside the timed region.  Every input (X 128 MiB, weights 361 MiB per
 layer) is larger than L2 and each layer has its own weights, so no L2 flush is
 needed between iterations.
 
 Under torchrun (N > 1): tensor parallel over d_ffn (strided neuron shards,
-replicated predictor, sharded compensator) with one NCCL all-reduce of each
-layer's output; scaling "strong" (total work fixed).
+replicated predictor, sharded compensator) with one all-reduce of each layer's
+output -- NCCL, or with `--collective fused` the peer-memory kernel that also
+adds the residual (tp.PeerBuffers); scaling "strong" (total work fixed).
+`--parallel dp`: one prompt per GPU, no collective; scaling "weak".
+The TTFT leg (N = 1) times the full 32-layer prefill (prefill.py) in the
+predicted and dense modes.
 
 `--impl reference` times the reference's own CPU implementation (the
 unmodified `sparseprefill` package from baseline/_ref when present, else the
