@@ -62,8 +62,6 @@ __global__ void __launch_bounds__(kNormThreads, 2)
                    float* __restrict__ out_f32, const float* __restrict__ query, float sqrt_d,
                    float* __restrict__ logits, int logit_row0, int logit_row1) {
   __shared__ double red[kNormThreads / 32];
-  pdl_wait();
-  pdl_trigger();
   const int nv = d / 4;
   double gd[kMaxV][4], qd[kMaxV][4];
 #pragma unroll
@@ -76,6 +74,10 @@ __global__ void __launch_bounds__(kNormThreads, 2)
     gd[j][0] = w.x; gd[j][1] = w.y; gd[j][2] = w.z; gd[j][3] = w.w;
     qd[j][0] = q.x; qd[j][1] = q.y; qd[j][2] = q.z; qd[j][3] = q.w;
   }
+  // gain and query are parameters, not the predecessor's output: widen them while the
+  // predecessor (the previous layer's down projection) drains, then wait for it
+  pdl_wait();
+  pdl_trigger();
   auto load_row = [&](int row, float4 (&v)[kMaxV]) {
     const float4* xr = reinterpret_cast<const float4*>(x + static_cast<size_t>(row) * d);
 #pragma unroll
