@@ -23,7 +23,9 @@ needed between iterations.
 Under torchrun (N > 1): tensor parallel over d_ffn (strided neuron shards,
 replicated predictor, sharded compensator) with one all-reduce of each layer's
 output -- NCCL, or with `--collective fused` the peer-memory kernel that also
-adds the residual (tp.PeerBuffers); scaling "strong" (total work fixed).
+adds the residual (tp.PeerBuffers), or with `--collective overlap` that kernel
+draining blocks while the down projection still runs (PeerBuffers.layer_overlap);
+scaling "strong" (total work fixed).
 `--parallel dp`: one prompt per GPU, no collective; scaling "weak".
 The TTFT leg (N = 1) times the full 32-layer prefill (prefill.py) in the
 predicted and dense modes.
@@ -377,7 +379,7 @@ def run_gpu(args, rank: int, world: int) -> None:
     gain = torch.ones(d, device=dev)            # ffn_norm gains (ones, synthetic.py:41)
     lg = torch.empty((T,), dtype=torch.float32, device=dev)
     peers = None
-    if tp > 1 and args.collective == "fused":
+    if tp > 1 and args.collective in ("fused", "overlap"):
         # fused completion: partial Y -> peer-memory reduce + residual add (tp.PeerBuffers)
         from paper_2602_00397_b200.tp import PeerBuffers
         peers = PeerBuffers(T, d, dev, with_xnext=False)
@@ -391,6 +393,9 @@ def run_gpu(args, rank: int, world: int) -> None:
             rmsnorm(res, gain, out=xb, predictor=dp, logits=lg)
             if tp == 1:
                 ff.sparse_ffn_layer(xb, packed, dp, k, out=res, residual=res, logits_in=lg,
+                                    workspace=ws)
+            elif args.collective == "overlap":
+                peers.layer_overlap(xb, packed, dp, k, residual=res, logits_in=lg,
                                     workspace=ws)
             elif peers is not None:
                 ff.sparse_ffn_layer(xb, packed, dp, k, out=peers.partial, logits_in=lg,
@@ -565,8 +570,9 @@ def main():
     ap.add_argument("--skip-dense", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-ttft", action="store_true")
-    ap.add_argument("--collective", default="nccl", choices=["nccl", "fused"],
-                    help="TP completion: NCCL all-reduce, or the fused peer-memory kernel")
+    ap.add_argument("--collective", default="nccl", choices=["nccl", "fused", "overlap"],
+                    help="TP completion: NCCL all-reduce, the fused peer-memory kernel, or "
+                         "that kernel overlapped with the down projection block by block")
     ap.add_argument("--parallel", default="tp", choices=["tp", "dp"],
                     help="N>1: tensor parallel over d_ffn (one prompt) or data parallel "
                          "(one prompt per GPU)")

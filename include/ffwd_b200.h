@@ -253,6 +253,37 @@ FFWD_API int ffwd_allreduce_residual(const float* const* partials, float* const*
                                      void* const* xnexts, unsigned* const* flags, int n_ranks,
                                      int rank, const float* residual, int T, int d,
                                      unsigned epoch, int max_ctas, void* stream);
+/*
+ * One tensor-parallel layer (as ffwd_ffn_layer2 with tp_size ranks) whose completion is
+ * overlapped with the down projection: this rank's K3 writes its partial Y into
+ * partials[tp_rank] and publishes, per 128-token block, how many column tiles are done
+ * (y_done[tp_rank][b] += 1 per tile, system-scope release); a completion kernel on
+ * `comm_stream` (comm_ctas CTAs, default 16) starts when this rank's up projection
+ * retires and, block by block in the plan's raster order, waits for y_done[p][b] >=
+ * y_epoch * (d / 256) on every rank p and then does ffwd_allreduce_residual's work for
+ * its 1/N of the block's rows.  So the reduce-scatter + all-gather of block b over
+ * NVLink runs while K3 still computes later blocks ("chunk over block
+ * groups and overlap").  `stream` waits for the completion before returning work to the
+ * caller.  y_done: caller-owned u32 [ceil(T/128)] per rank, zeroed once and never reset;
+ * y_epoch counts the overlapped layers run on those counters (1, 2, ...); `epoch` is
+ * ffwd_allreduce_residual's flag epoch.  xnexts must not alias x_bf16 (peers write the
+ * next layer's input while this rank may still read this one).  Replaces
+ * engine.py:294-308 (sparse FFN, compensator, residual) with the TP all-reduce of
+ * SURVEY 8(e) fused in.
+ */
+FFWD_API int ffwd_ffn_layer_tp_overlap(const void* x_bf16, int T, int d, const void* wgu_t,
+                                       const void* wd, int f_local, int rc_local,
+                                       const float* query, const float* w1, const float* w2,
+                                       int r, int f_global, int k, int dense_first_last,
+                                       int has_comp, int tp_rank, int tp_size,
+                                       int32_t* idx_global, int ld_idx_global,
+                                       const float* x_pred_f32, const float* logits_in,
+                                       const float* const* partials, float* const* outs,
+                                       void* const* xnexts, unsigned* const* flags,
+                                       unsigned* const* y_done, const float* residual,
+                                       unsigned epoch, unsigned y_epoch, int comm_ctas,
+                                       void* workspace, size_t workspace_bytes, void* stream,
+                                       void* comm_stream);
 /* CUDA IPC: the 64-byte handle of the allocation holding dev_ptr plus dev_ptr's
  * offset in it; ffwd_ipc_open maps a peer's allocation (add the offset). */
 FFWD_API int ffwd_ipc_get_handle(void* dev_ptr, void* handle_out, size_t* offset_out);

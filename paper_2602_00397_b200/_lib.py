@@ -68,6 +68,11 @@ SIGNATURES = {
                                   ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_uint64)]),
     "ffwd_allreduce_residual": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_int, _vp, _c_int, _c_int,
                                          ctypes.c_uint, _c_int, _vp]),
+    "ffwd_ffn_layer_tp_overlap": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _vp,
+                                           _vp, _vp, _c_int, _c_int, _c_int, _c_int, _c_int,
+                                           _c_int, _c_int, _vp, _c_int, _vp, _vp, _vp, _vp, _vp,
+                                           _vp, _vp, _vp, ctypes.c_uint, ctypes.c_uint, _c_int,
+                                           _vp, _c_size, _vp, _vp]),
     "ffwd_ipc_get_handle": (_c_int, [_vp, _vp, ctypes.POINTER(_c_size)]),
     "ffwd_ipc_open": (_c_int, [_vp, ctypes.POINTER(_vp)]),
     "ffwd_ipc_close": (_c_int, [_vp]),

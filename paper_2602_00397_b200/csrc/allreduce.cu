@@ -64,47 +64,68 @@ __device__ __forceinline__ void wait_flags(const unsigned* f, int n, unsigned ep
   }
 }
 
-__global__ void __launch_bounds__(kArThreads) allreduce_residual_kernel(ArArgs a) {
-  const int n = a.n, r = a.rank;
-  // ---- arrive: this rank's partial (written by K3 before this kernel) is complete
-  if (blockIdx.x == 0 && threadIdx.x < n) {
-    __threadfence_system();
-    st_release_sys(a.flags[threadIdx.x] + r, a.epoch);
-  }
-  if (threadIdx.x == 0) wait_flags(a.flags[r], n, a.epoch);
-  __syncthreads();
+// out_p[rows] = residual[rows] + sum_q partial_q[rows] on every rank p, rows [r0, r1),
+// grid-strided over `ctas` CTAs starting at `cta`.  Each thread keeps kUnroll float4 of
+// every source in flight (peer loads over NVLink take microseconds: the kernel is bound
+// by bytes in flight, not by bandwidth, with one load per thread).
+constexpr int kUnroll = 4;
 
-  // ---- reduce my row slice, fused residual add, all-gather stores
-  const int r0 = static_cast<int>((static_cast<long long>(a.T) * r) / n);
-  const int r1 = static_cast<int>((static_cast<long long>(a.T) * (r + 1)) / n);
+__device__ __forceinline__ void reduce_rows(const ArArgs& a, int r0, int r1, int cta, int ctas) {
+  const int n = a.n, r = a.rank;
   const size_t base = static_cast<size_t>(r0) * a.d;
   const size_t nvec = static_cast<size_t>(r1 - r0) * a.d / 4;  // d % 4 == 0
-  for (size_t i = static_cast<size_t>(blockIdx.x) * kArThreads + threadIdx.x; i < nvec;
-       i += static_cast<size_t>(gridDim.x) * kArThreads) {
-    const size_t e = base + 4 * i;
-    float4 s = *reinterpret_cast<const float4*>(a.residual + e);
+  const size_t stride = static_cast<size_t>(ctas) * kArThreads;
+  for (size_t i0 = static_cast<size_t>(cta) * kArThreads + threadIdx.x; i0 < nvec;
+       i0 += stride * kUnroll) {
+    float4 s[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const size_t i = i0 + u * stride;
+      s[u] = i < nvec ? *reinterpret_cast<const float4*>(a.residual + base + 4 * i)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     for (int p = 0; p < n; ++p) {  // fixed rank order: identical sums on every rank
-      const float4 v = __ldcs(reinterpret_cast<const float4*>(a.partial[p] + e));
-      s.x += v.x;
-      s.y += v.y;
-      s.z += v.z;
-      s.w += v.w;
+      float4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const size_t i = i0 + u * stride;
+        v[u] = i < nvec ? __ldcg(reinterpret_cast<const float4*>(a.partial[p] + base + 4 * i))
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        s[u].x += v[u].x;
+        s[u].y += v[u].y;
+        s[u].z += v[u].z;
+        s[u].w += v[u].w;
+      }
     }
-    uint2 pk;
-    if (a.xnext[0] != nullptr) {
-      const __nv_bfloat162 lo = __floats2bfloat162_rn(s.x, s.y);
-      const __nv_bfloat162 hi = __floats2bfloat162_rn(s.z, s.w);
-      pk.x = *reinterpret_cast<const uint32_t*>(&lo);
-      pk.y = *reinterpret_cast<const uint32_t*>(&hi);
-    }
-    for (int p = 0; p < n; ++p) {
-      const int q = (r + p) % n;  // stagger the destinations across ranks
-      __stcg(reinterpret_cast<float4*>(a.out[q] + e), s);
-      if (a.xnext[0] != nullptr) __stcg(reinterpret_cast<uint2*>(a.xnext[q] + e), pk);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const size_t i = i0 + u * stride;
+      if (i >= nvec) break;
+      const size_t e = base + 4 * i;
+      uint2 pk;
+      if (a.xnext[0] != nullptr) {
+        const __nv_bfloat162 lo = __floats2bfloat162_rn(s[u].x, s[u].y);
+        const __nv_bfloat162 hi = __floats2bfloat162_rn(s[u].z, s[u].w);
+        pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+      }
+      for (int p = 0; p < n; ++p) {
+        const int q = (r + p) % n;  // stagger the destinations across ranks
+        __stcg(reinterpret_cast<float4*>(a.out[q] + e), s[u]);
+        if (a.xnext[0] != nullptr) __stcg(reinterpret_cast<uint2*>(a.xnext[q] + e), pk);
+      }
     }
   }
+}
 
-  // ---- depart: the last CTA publishes "rank r's slice is written" on every peer
+// The last CTA of rank r (grid-wide counter) publishes "rank r's rows are written" on
+// every peer; every CTA then waits for all peers' departures, so when the kernel retires
+// on rank r no peer still reads rank r's partial or writes rank r's output.
+__device__ __forceinline__ void depart(const ArArgs& a) {
+  const int n = a.n, r = a.rank;
   __syncthreads();
   __shared__ bool last;
   if (threadIdx.x == 0) {
@@ -118,6 +139,64 @@ __global__ void __launch_bounds__(kArThreads) allreduce_residual_kernel(ArArgs a
   if (last && threadIdx.x < n) st_release_sys(a.flags[threadIdx.x] + n + r, a.epoch);
   if (threadIdx.x == 0) wait_flags(a.flags[r] + n, n, a.epoch);
   __syncthreads();
+}
+
+__global__ void __launch_bounds__(kArThreads) allreduce_residual_kernel(ArArgs a) {
+  const int n = a.n, r = a.rank;
+  // ---- arrive: this rank's partial (written by K3 before this kernel) is complete
+  if (blockIdx.x == 0 && threadIdx.x < n) {
+    __threadfence_system();
+    st_release_sys(a.flags[threadIdx.x] + r, a.epoch);
+  }
+  if (threadIdx.x == 0) wait_flags(a.flags[r], n, a.epoch);
+  __syncthreads();
+
+  // ---- reduce my row slice, fused residual add, all-gather stores
+  const int r0 = static_cast<int>((static_cast<long long>(a.T) * r) / n);
+  const int r1 = static_cast<int>((static_cast<long long>(a.T) * (r + 1)) / n);
+  reduce_rows(a, r0, r1, blockIdx.x, gridDim.x);
+
+  depart(a);
+}
+
+// Overlapped with the down projection: the plan's raster order (dense blocks first, then
+// the predicted range; plan.cu order_to_block) is the order K3 finishes blocks in, so CTA c
+// takes blocks o = c, c + G, ... of that order, waits until every rank's K3 has published
+// all column tiles of the block (ydone counters, system-scope release in the K3
+// epilogue), and reduces this rank's 1/N of the block's rows -- the transfer of block b
+// runs while K3 still computes later blocks.
+struct ArOvArgs {
+  ArArgs base;
+  const unsigned* ydone[kMaxRanks];
+  unsigned target;
+  int sparse_begin, sparse_count;
+};
+
+__global__ void __launch_bounds__(kArThreads) allreduce_overlap_kernel(ArOvArgs ov) {
+  const ArArgs& a = ov.base;
+  const int n = a.n, r = a.rank;
+  const int n_blk = (a.T + kBlockTokens - 1) / kBlockTokens;
+  const int n_dense = n_blk - ov.sparse_count;
+  for (int o = blockIdx.x; o < n_blk; o += gridDim.x) {
+    const int b = o < ov.sparse_begin ? o
+                  : o < n_dense      ? ov.sparse_begin + ov.sparse_count + (o - ov.sparse_begin)
+                                     : ov.sparse_begin + (o - n_dense);
+    if (threadIdx.x == 0) {
+      for (int q = 0; q < n; ++q) {
+        long long spins = 0;
+        while (static_cast<int>(ld_acquire_sys(ov.ydone[q] + b) - ov.target) < 0) {
+          __nanosleep(128);
+          if (++spins > (1ll << 24)) __trap();  // a rank's K3 never finished block b
+        }
+      }
+    }
+    __syncthreads();
+    const int t0 = b * kBlockTokens;
+    const int nt = min(kBlockTokens, a.T - t0);
+    reduce_rows(a, t0 + nt * r / n, t0 + nt * (r + 1) / n, 0, 1);
+    __syncthreads();
+  }
+  depart(a);
 }
 
 }  // namespace
@@ -142,6 +221,41 @@ cudaError_t launch_allreduce_residual(const float* const* partial, float* const*
   a.epoch = epoch;
   // every CTA spins at the end, so the grid must be co-resident: one wave
   allreduce_residual_kernel<<<max_ctas, kArThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace ffwd
+
+namespace ffwd {
+
+cudaError_t launch_allreduce_overlap(const float* const* partial, float* const* out,
+                                     void* const* xnext, unsigned* const* flags,
+                                     const unsigned* const* ydone, int n, int rank,
+                                     const float* residual, int T, int d, unsigned epoch,
+                                     unsigned target, int sparse_begin, int sparse_count,
+                                     int max_ctas, cudaStream_t s) {
+  if (n < 1 || n > kMaxRanks) return cudaErrorInvalidValue;
+  ArOvArgs ov{};
+  ArArgs& a = ov.base;
+  for (int p = 0; p < n; ++p) {
+    a.partial[p] = partial[p];
+    a.out[p] = out[p];
+    a.xnext[p] = xnext ? static_cast<__nv_bfloat16*>(xnext[p]) : nullptr;
+    a.flags[p] = flags[p];
+    ov.ydone[p] = ydone[p];
+  }
+  a.residual = residual;
+  a.n = n;
+  a.rank = rank;
+  a.T = T;
+  a.d = d;
+  a.epoch = epoch;
+  ov.target = target;
+  ov.sparse_begin = sparse_begin;
+  ov.sparse_count = sparse_count;
+  // few CTAs: they spin beside K3 (one K3 CTA per SM leaves room for one of these) and
+  // must all be resident for the final departure barrier
+  allreduce_overlap_kernel<<<max_ctas, kArThreads, 0, s>>>(ov);
   return cudaGetLastError();
 }
 

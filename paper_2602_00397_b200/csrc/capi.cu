@@ -213,7 +213,8 @@ int run_ffn(const void* x, int T, int d, const void* wgu_t, const void* wd, int 
             int rc_local, const Ffn& w, const int32_t* idx, int ld_idx, int sparse_begin,
             int sparse_count, const int32_t* counts, int k_shared, int idx_shared, int has_comp,
             float* y, const float* residual, void* x_next, cudaStream_t s,
-            bool up_only = false) {
+            bool up_only = false, unsigned* y_done = nullptr,
+            cudaEvent_t after_up = nullptr) {
   const int n_blk = (T + kBlockTokens - 1) / kBlockTokens;
   PlanArgs pa{};
   pa.T = T;
@@ -265,11 +266,13 @@ int run_ffn(const void* x, int T, int d, const void* wgu_t, const void* wd, int 
   ga.num_sms = num_sms();
   ga.bn_down = bn_for(d);
   ga.blk_done = pa.blk_done;
+  ga.y_done = y_done;
   {
     StageTimer tm(kUp, s);
     FFWD_CUDA(launch_up_proj(ga, s), "up_proj");
   }
   if (up_only) return FFWD_OK;  // H only (oracle scoring)
+  if (after_up) FFWD_CUDA(cudaEventRecord(after_up, s), "event record");
   {
     StageTimer tm(kDown, s);
     FFWD_CUDA(launch_down_proj(ga, s), "down_proj");
@@ -672,6 +675,85 @@ int ffwd_allreduce_residual(const float* const* partials, float* const* outs,
   FFWD_CUDA(launch_allreduce_residual(partials, outs, xnexts, flags, n_ranks, rank, residual, T,
                                       d, epoch, ctas, static_cast<cudaStream_t>(stream)),
             "allreduce_residual");
+  return FFWD_OK;
+}
+
+int ffwd_ffn_layer_tp_overlap(const void* x_bf16, int T, int d, const void* wgu_t,
+                              const void* wd, int f_local, int rc_local, const float* query,
+                              const float* w1, const float* w2, int r, int f_global, int k,
+                              int dense_first_last, int has_comp, int tp_rank, int tp_size,
+                              int32_t* idx_global, int ld_idx_global, const float* x_pred_f32,
+                              const float* logits_in, const float* const* partials,
+                              float* const* outs, void* const* xnexts, unsigned* const* flags,
+                              unsigned* const* y_done, const float* residual, unsigned epoch,
+                              unsigned y_epoch, int comm_ctas, void* workspace,
+                              size_t workspace_bytes, void* stream, void* comm_stream) {
+  g_err.clear();
+  int rc = check_common(T, d, f_global, k);
+  if (rc) return rc;
+  if ((rc = check_gemm_shapes(d, f_local))) return rc;
+  if (tp_size < 1 || tp_size > 8 || tp_rank < 0 || tp_rank >= tp_size)
+    return fail(FFWD_ERR_VALIDATION, "bad tensor-parallel rank %d of %d (1..8 ranks)", tp_rank,
+                tp_size);
+  if (f_local != (f_global - tp_rank + tp_size - 1) / tp_size)
+    return fail(FFWD_ERR_VALIDATION, "f_local=%d is not rank %d's strided share of d_ffn=%d",
+                f_local, tp_rank, f_global);
+  if (has_comp && rc_local < 1) return fail(FFWD_ERR_VALIDATION, "compensator width must be >= 1");
+  if (!partials || !outs || !flags || !y_done || !residual)
+    return fail(FFWD_ERR_VALIDATION,
+                "overlapped completion needs partial, out, flag, y_done and residual pointers");
+  for (int p = 0; p < tp_size; ++p)
+    if (!partials[p] || !outs[p] || !flags[p] || !y_done[p] || (xnexts && !xnexts[p]))
+      return fail(FFWD_ERR_VALIDATION, "null peer pointer for rank %d", p);
+  if (xnexts && xnexts[tp_rank] == x_bf16)
+    return fail(FFWD_ERR_VALIDATION, "x_next must not alias the layer input (peers write it "
+                                     "while this rank may still read it)");
+  if (workspace_bytes <
+      ffwd_layer_workspace_bytes(T, d, f_global, f_local, rc_local, r, k, dense_first_last, tp_size))
+    return fail(FFWD_ERR_VALIDATION, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaStream_t cs = static_cast<cudaStream_t>(comm_stream);
+  if (cs == s) return fail(FFWD_ERR_VALIDATION, "the completion needs its own stream");
+  static thread_local cudaEvent_t ev_up = nullptr, ev_done = nullptr;
+  if (!ev_up) {
+    FFWD_CUDA(cudaEventCreateWithFlags(&ev_up, cudaEventDisableTiming), "event create");
+    FFWD_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming), "event create");
+  }
+  int b0, nb;
+  layer_split(T, k, f_global, dense_first_last, &b0, &nb);
+  const int kmax = local_kmax(k, f_local);
+  Carve c(workspace);
+  Pred p = carve_pred(c, nb, d, r, f_global, true);
+  Ffn w = carve_ffn(c, T, d, f_local, rc_local, kmax, nb, rup(kmax, 4));
+  if (nb > 0) {
+    if (d % 8 != 0) return fail(FFWD_ERR_UNSUPPORTED, "predictor needs d_model %% 8 == 0");
+    if (idx_global && ld_idx_global < k) return fail(FFWD_ERR_VALIDATION, "ld_idx_global < k");
+    rc = x_pred_f32 ? run_predictor(x_pred_f32, true, T, d, b0, nb, query, w1, w2, r, f_global,
+                                    p, p.scores, s, logits_in)
+                    : run_predictor(x_bf16, false, T, d, b0, nb, query, w1, w2, r, f_global, p,
+                                    p.scores, s, logits_in);
+    if (rc) return rc;
+    StageTimer tm(kTopk, s);
+    FFWD_CUDA(launch_topk(p.scores, nb, f_global, k, tp_rank, tp_size, idx_global, ld_idx_global,
+                          w.idx_local, w.ld_local, w.counts, s),
+              "topk");
+  }
+  // K3 publishes per-block tile counts; the completion starts once K2 retired (its CTAs
+  // then sit beside K3's, one K3 CTA per SM leaving the room) and drains blocks as they
+  // finish on every rank
+  rc = run_ffn(x_bf16, T, d, wgu_t, wd, f_local, rc_local, w, w.idx_local, w.ld_local, b0, nb,
+               tp_size > 1 ? w.counts : nullptr, k, 0, has_comp,
+               const_cast<float*>(partials[tp_rank]), nullptr, nullptr, s, false,
+               y_done[tp_rank], ev_up);
+  if (rc) return rc;
+  FFWD_CUDA(cudaStreamWaitEvent(cs, ev_up, 0), "stream wait");
+  const unsigned target = y_epoch * static_cast<unsigned>(d / bn_for(d));
+  FFWD_CUDA(launch_allreduce_overlap(partials, outs, xnexts, flags, y_done, tp_size, tp_rank,
+                                     residual, T, d, epoch, target, b0, nb,
+                                     comm_ctas > 0 ? comm_ctas : 16, cs),
+            "allreduce_overlap");
+  FFWD_CUDA(cudaEventRecord(ev_done, cs), "event record");
+  FFWD_CUDA(cudaStreamWaitEvent(s, ev_done, 0), "stream wait");
   return FFWD_OK;
 }
 

@@ -279,6 +279,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&sm.bar->tempty[acc]);
+      if (a.y_done != nullptr && tl.kind == 2) {
+        // publish "one more column tile of block b is in Y" to the overlapped TP
+        // completion, which reads Y from peer GPUs: system-scope release
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (ew == 0 && lane == 0) {
+          __threadfence_system();
+          atomicAdd(a.y_done + tl.b, 1u);
+        }
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }

@@ -57,6 +57,15 @@ cudaError_t launch_allreduce_residual(const float* const* partial, float* const*
                                       void* const* xnext, unsigned* const* flags, int n,
                                       int rank, const float* residual, int T, int d,
                                       unsigned epoch, int max_ctas, cudaStream_t s);
+// The same completion overlapped with the down projection: block by block (in the plan's
+// raster order) once every rank's K3 has published all of the block's column tiles
+// (ydone[p][b] reaching `target`, a running count).
+cudaError_t launch_allreduce_overlap(const float* const* partial, float* const* out,
+                                     void* const* xnext, unsigned* const* flags,
+                                     const unsigned* const* ydone, int n, int rank,
+                                     const float* residual, int T, int d, unsigned epoch,
+                                     unsigned target, int sparse_begin, int sparse_count,
+                                     int max_ctas, cudaStream_t s);
 // sparse.hidden_column_scores over bf16 H [n_blk*128 x hcols] -> scores [n_blk x f]
 cudaError_t launch_hidden_scores(const void* h, bool is_f32, int ld, int T, int f,
                                  float* scores, cudaStream_t s);
@@ -116,6 +125,8 @@ struct GemmArgs {
   int num_sms;
   int bn_down;
   int* blk_done;  // nullable: block-granular K2 -> K3 dependency (per-block done tiles)
+  unsigned* y_done;  // nullable: per-block finished down tiles, released at system scope
+                     // (the overlapped TP completion consumes blocks as they finish)
 };
 
 cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s);

@@ -8,7 +8,10 @@ collective is needed before the FFN) and keeps its local subset.  Each rank's
 down projection yields a partial Y; one all-reduce (sum) per layer completes
 it -- either NCCL (``allreduce_partial``) or the fused peer-memory kernel
 (``PeerBuffers.complete``: reduce-scatter + all-gather over NVLink in one pass,
-with the residual add and the next layer's bf16 input fused in).  Independent
+with the residual add and the next layer's bf16 input fused in), or that same
+completion overlapped with the down projection block by block
+(``PeerBuffers.layer_overlap``: K3 publishes per-block tile counts, the completion
+drains each block as soon as every rank has finished it).  Independent
 prompts are data parallel and need no collective at all.
 """
 
@@ -20,9 +23,11 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+from . import _dev, _lib
 from .compensator import CompensatorParams
 from .errors import ValidationError
-from .layer import PackedLayer, pack_layer, shard_comp_cols, shard_neurons, sparse_ffn_layer
+from .layer import (BLOCK, PackedLayer, layer_workspace_bytes, pack_layer, shard_comp_cols,
+                    shard_neurons, sparse_ffn_layer)
 from .predictor import DevicePredictor
 
 
@@ -114,6 +119,56 @@ def allreduce_residual_fused(partials, outs, flags, rank: int, residual: torch.T
         _dev.stream_handle(residual.device)), "allreduce_residual")
 
 
+def _ptr_array(items):
+    import ctypes
+    arr = (ctypes.c_void_p * len(items))()
+    for i, t in enumerate(items):
+        arr[i] = t if isinstance(t, int) else t.data_ptr()
+    return arr
+
+
+def sparse_ffn_layer_tp_overlap(x, packed: PackedLayer, predictor: DevicePredictor, k: int, *,
+                                partials, outs, flags, y_done, residual: torch.Tensor,
+                                epoch: int, y_epoch: int, xnexts=None,
+                                dense_first_last: bool = True, has_comp: bool = True,
+                                comm_ctas: int = 16, x_pred_f32=None, logits_in=None,
+                                workspace: torch.Tensor | None = None, comm_stream=None):
+    """One rank's TP layer with the completion overlapped (``ffwd_ffn_layer_tp_overlap``).
+
+    The down projection writes this rank's partial Y into ``partials[rank]`` and counts
+    finished column tiles per block in ``y_done[rank]``; a completion kernel on
+    ``comm_stream`` sums each block over the ranks (fixed rank order, + ``residual``)
+    into every rank's ``outs`` (and ``xnexts``) while later blocks are still computed.
+    Peer lists hold one CUDA tensor (single-process emulation) or device pointer
+    (``PeerBuffers``) per rank.  The current stream waits for the completion.
+    """
+    from .layer import _x_bf16
+    dev = packed.device
+    xb = _x_bf16(x, dev)
+    T, d = xb.shape
+    n = packed.tp_size
+    if not (len(partials) == len(outs) == len(flags) == len(y_done) == n) or (
+            xnexts is not None and len(xnexts) != n):
+        raise ValidationError("one partial, out, flag, y_done (and x_next) buffer per rank")
+    if tuple(residual.shape) != (T, d) or residual.dtype != torch.float32:
+        raise ValidationError(f"residual must be f32 {(T, d)}")
+    ws_n = layer_workspace_bytes(T, packed, predictor.r, k, dense_first_last)
+    ws = workspace if workspace is not None and workspace.numel() >= ws_n else \
+        _dev.workspace(dev, ws_n)
+    cs = comm_stream if comm_stream is not None else torch.cuda.Stream(dev)
+    lib = _dev.lib_for(dev)
+    _lib.check(lib.ffwd_ffn_layer_tp_overlap(
+        xb.data_ptr(), T, d, packed.wgu_t.data_ptr(), packed.wd.data_ptr(), packed.f_local,
+        packed.rc_local, predictor.query.data_ptr(), predictor.w1.data_ptr(),
+        predictor.w2.data_ptr(), predictor.r, predictor.f, k, int(dense_first_last),
+        int(has_comp and packed.rc_local > 0), packed.tp_rank, n, None, 0,
+        _dev.ptr(x_pred_f32), _dev.ptr(logits_in), _ptr_array(partials), _ptr_array(outs),
+        _ptr_array(xnexts) if xnexts is not None else None, _ptr_array(flags),
+        _ptr_array(y_done), residual.data_ptr(), int(epoch) & 0xFFFFFFFF,
+        int(y_epoch) & 0xFFFFFFFF, comm_ctas, ws.data_ptr(), ws.numel(),
+        _dev.stream_handle(dev), cs.cuda_stream), "ffn_layer_tp_overlap")
+
+
 class PeerBuffers:
     """Per-rank partial-Y, residual-stream and flag buffers shared over CUDA IPC, for the
     fused TP completion (one process per GPU, NVLink peer access)."""
@@ -129,9 +184,11 @@ class PeerBuffers:
         self.out = torch.empty((T, d), dtype=torch.float32, device=dev)
         self.xnext = torch.empty((T, d), dtype=torch.bfloat16, device=dev) if with_xnext else None
         self.flags = torch.zeros((2 * self.world + 1,), dtype=torch.int32, device=dev)
+        # per-block finished down tiles (overlapped completion); never reset
+        self.y_done = torch.zeros((-(-T // BLOCK),), dtype=torch.int32, device=dev)
         lib = _lib.load_library()
         mine = []
-        for t in (self.partial, self.out, self.xnext, self.flags):
+        for t in (self.partial, self.out, self.xnext, self.flags, self.y_done):
             if t is None:
                 mine.append(None)
                 continue
@@ -142,10 +199,11 @@ class PeerBuffers:
         allh = [None] * self.world
         dist.all_gather_object(allh, mine, group=group)
         self._opened = []
-        self.peer = {"partial": [], "out": [], "xnext": [], "flags": []}
+        self.peer = {"partial": [], "out": [], "xnext": [], "flags": [], "y_done": []}
         for p in range(self.world):
-            for key, t, hv in zip(("partial", "out", "xnext", "flags"),
-                                  (self.partial, self.out, self.xnext, self.flags), allh[p]):
+            for key, t, hv in zip(("partial", "out", "xnext", "flags", "y_done"),
+                                  (self.partial, self.out, self.xnext, self.flags, self.y_done),
+                                  allh[p]):
                 if hv is None:
                     continue
                 if p == self.rank:
@@ -156,6 +214,8 @@ class PeerBuffers:
                 self._opened.append(base.value)
                 self.peer[key].append(base.value + hv[1])
         self.epoch = 0
+        self.y_epoch = 0
+        self.comm_stream = torch.cuda.Stream(dev)
         torch.cuda.synchronize(dev)
         dist.barrier(group=group)
 
@@ -167,6 +227,23 @@ class PeerBuffers:
                                  self.rank, residual, self.epoch,
                                  self.peer["xnext"] if self.xnext is not None else None,
                                  max_ctas)
+        return self.out
+
+    def layer_overlap(self, x, packed: PackedLayer, predictor: DevicePredictor, k: int,
+                      residual: torch.Tensor, dense_first_last: bool = True,
+                      comm_ctas: int = 16, **kw) -> torch.Tensor:
+        """This rank's layer with the completion overlapped with its down projection:
+        afterwards every rank's ``out`` holds residual + the full FFN output (``xnext``
+        its bf16 copy; it must not be the layer input ``x``)."""
+        self.epoch += 1
+        self.y_epoch += 1
+        sparse_ffn_layer_tp_overlap(
+            x, packed, predictor, k, partials=self.peer["partial"], outs=self.peer["out"],
+            flags=self.peer["flags"], y_done=self.peer["y_done"], residual=residual,
+            epoch=self.epoch, y_epoch=self.y_epoch,
+            xnexts=self.peer["xnext"] if self.xnext is not None else None,
+            dense_first_last=dense_first_last, comm_ctas=comm_ctas,
+            comm_stream=self.comm_stream, **kw)
         return self.out
 
     def close(self):

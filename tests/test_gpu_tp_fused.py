@@ -92,6 +92,63 @@ def test_fused_completion_of_sharded_layer(ff):
         assert rel <= 5e-3, f"TP={n}: rel-L2 of the FFN part {rel:.2e}"
 
 
+@pytest.mark.parametrize("n", [2, 4])
+def test_overlapped_completion_of_sharded_layer(ff, n):
+    """The completion overlapped with the down projection (``ffwd_ffn_layer_tp_overlap``):
+    every emulated rank runs its whole layer on its own stream with the completion on a
+    second stream, K3 publishing per-block tile counts the completions drain block by
+    block.  Bit-exact against the sequential path (sharded layer, then the fused
+    completion: same partials, same rank-order sums) on every rank, over three layers
+    reusing the counters and flags."""
+    from paper_2602_00397_b200.layer import layer_workspace_bytes
+    from paper_2602_00397_b200.tp import sparse_ffn_layer_tp_overlap
+    from tests.fixtures import load_case
+    c = load_case("cfg1")
+    lw, pred, comp = c["lw"], c["pred"], ff.CompensatorParams(**c["comp"])
+    xb = torch.from_numpy(c["x"]).cuda().to(torch.bfloat16)
+    T, d = xb.shape
+    k = int(c["k"])
+    dp = ff.DevicePredictor.from_params(ff.PredictorParams(**pred), "cuda")
+    res0 = torch.randn((T, d), device="cuda")
+    packs = [ff.pack_layer(lw["w_gate"], lw["w_up"], lw["w_down"], comp, device="cuda",
+                           tp_rank=r, tp_size=n) for r in range(n)]
+    # sequential reference: partials, then the (non-overlapped) fused completion
+    partials = [ff.sparse_ffn_layer(xb, pk, dp, k) for pk in packs]
+    want = [res0.clone() for _ in range(n)]
+    fl = [torch.zeros(2 * n + 1, dtype=torch.int32, device="cuda") for _ in range(n)]
+    _run_ranks(partials, want, fl, want, 1)
+
+    ws = [torch.empty(layer_workspace_bytes(T, packs[r], dp.r, k, True), dtype=torch.uint8,
+                      device="cuda") for r in range(n)]
+    part = [torch.empty((T, d), device="cuda") for _ in range(n)]
+    flags = [torch.zeros(2 * n + 1, dtype=torch.int32, device="cuda") for _ in range(n)]
+    y_done = [torch.zeros(-(-T // 128), dtype=torch.int32, device="cuda") for _ in range(n)]
+    main = [torch.cuda.Stream() for _ in range(n)]
+    comm = [torch.cuda.Stream() for _ in range(n)]
+    cur = torch.cuda.current_stream()
+    for layer in (1, 2, 3):
+        outs = [res0.clone() for _ in range(n)]
+        xn = [torch.empty((T, d), dtype=torch.bfloat16, device="cuda") for _ in range(n)]
+        for s in main:
+            s.wait_stream(cur)
+        for r in range(n):
+            with torch.cuda.stream(main[r]):
+                sparse_ffn_layer_tp_overlap(
+                    xb, packs[r], dp, k, partials=part, outs=outs, flags=flags, y_done=y_done,
+                    residual=outs[r], epoch=layer, y_epoch=layer, xnexts=xn, comm_ctas=8,
+                    workspace=ws[r], comm_stream=comm[r])
+        for s in main:
+            cur.wait_stream(s)
+        torch.cuda.synchronize()
+        for r in range(n):
+            assert torch.equal(part[r], partials[r]), f"rank {r} partial differs"
+            assert torch.equal(outs[r], want[0]), f"layer {layer}: rank {r} output differs"
+            assert torch.equal(xn[r], want[0].to(torch.bfloat16))
+            assert int(y_done[r].min()) == int(y_done[r].max()) == layer * (d // (256 if d % 256 == 0 else 128 if d % 128 == 0 else 64))
+    for f in flags:
+        assert int(f[2 * n]) == 0
+
+
 def _ipc_worker(rank, world, port, q):
     import os
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -143,7 +200,8 @@ def test_peer_buffers_across_processes(ff):
     assert results == [(0, True, True), (1, True, True)]
 
 
-def test_bench_tensor_parallel_fused_path_runs(ff):
+@pytest.mark.parametrize("collective", ["fused", "overlap"])
+def test_bench_tensor_parallel_fused_path_runs(ff, collective):
     """bench.py under torchrun, 2 ranks, --collective fused, emulated on the one GPU (gloo
     for the host-side rendezvous, both ranks time-sliced on GPU 0): the TP sharding, the
     CUDA IPC peer buffers and the fused completion run end to end and the JSON line is
@@ -161,10 +219,10 @@ def test_bench_tensor_parallel_fused_path_runs(ff):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "2",
            "--config", "1b", "--layers", "2", "--steps", "2", "--warmup", "3",
-           "--collective", "fused"]
+           "--collective", collective]
     r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=400)
     assert r.returncode == 0, r.stderr[-3000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
     d = json.loads(line)
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "tp2"
-    assert d["config"]["collective"] == "fused" and d["value"] > 0
+    assert d["config"]["collective"] == collective and d["value"] > 0
