@@ -16,7 +16,8 @@ FFN-only stack without it overflows to inf by layer 6).  `value` = device time
 per step / 32 (ms per layer), inputs resident in HBM, uninstrumented (the
 per-kernel breakdown comes from a second, event-timed run); `e2e` = the same stack through the public API with the
 prompt's hidden states copied from pinned host memory and the result copied
-back inside the timed region.  Every input (X 128 MiB, weights 361 MiB per
+back inside the timed region, every step (the copies of step i+1 / i overlap step
+i's compute on a copy stream, double-buffered).  Every input (X 128 MiB, weights 361 MiB per
 layer) is larger than L2 and each layer has its own weights, so no L2 flush is
 needed between iterations.
 
@@ -445,21 +446,53 @@ def run_gpu(args, rank: int, world: int) -> None:
     fl.timing_enable(False)
     stages = fl.timing_read()
 
-    # ---- e2e through the public API with host buffers
+    # ---- e2e through the public API with host buffers.  Every step uploads its own input
+    # from pinned host memory and reads its result back; the copies run on a copy stream,
+    # double-buffered, so step i+1's upload and step i's readback overlap step i's compute
+    # (the first upload and the last readback are exposed inside the timed region).
     host_in = torch.empty((T, d), dtype=torch.float32, pin_memory=True)
     host_in.copy_(x0.cpu())
-    host_out = torch.empty_like(host_in, pin_memory=True)
+    host_out = [torch.empty_like(host_in, pin_memory=True) for _ in range(2)]
+    xd = [torch.empty((T, d), dtype=torch.float32, device=dev) for _ in range(2)]
+    yd = [torch.empty((T, d), dtype=torch.float32, device=dev) for _ in range(2)]
+    copy_s = torch.cuda.Stream(dev)
+    ev = {key: [torch.cuda.Event() for _ in range(2)] for key in ("in", "x_free", "y", "out")}
 
-    def e2e_step():
-        xd = host_in.to(dev, non_blocking=True)
-        stack(xd)
-        host_out.copy_(res, non_blocking=True)
+    def e2e_run(n):
+        cur = torch.cuda.current_stream(dev)
+        copy_s.wait_stream(cur)
+        with torch.cuda.stream(copy_s):
+            xd[0].copy_(host_in, non_blocking=True)
+            ev["in"][0].record(copy_s)
+        for i in range(n):
+            j = i % 2
+            if i + 1 < n:  # prefetch the next step's input into the other buffer
+                with torch.cuda.stream(copy_s):
+                    if i >= 1:
+                        copy_s.wait_event(ev["x_free"][1 - j])
+                    xd[1 - j].copy_(host_in, non_blocking=True)
+                    ev["in"][1 - j].record(copy_s)
+            cur.wait_event(ev["in"][j])
+            stack(xd[j])
+            ev["x_free"][j].record(cur)
+            if i >= 2:
+                cur.wait_event(ev["out"][j])  # step i-2's readback released yd[j]
+            yd[j].copy_(res)
+            ev["y"][j].record(cur)
+            with torch.cuda.stream(copy_s):
+                copy_s.wait_event(ev["y"][j])
+                host_out[j].copy_(yd[j], non_blocking=True)
+                ev["out"][j].record(copy_s)
+        cur.wait_stream(copy_s)
 
-    for _ in range(1):
-        e2e_step()
-    e2e_ms = timed(e2e_step, max(1, args.steps // 2))
+    e2e_run(2)
+    n_e2e = max(2, args.steps // 2)
+    e2e_ms = timed(lambda: e2e_run(n_e2e), 1) / n_e2e
+    torch.cuda.synchronize(dev)
+    if not torch.equal(host_out[(n_e2e - 1) % 2], res.cpu()):
+        raise RuntimeError("e2e readback differs from the device result")
     h2d = host_in.numel() * 4
-    d2h = host_out.numel() * 4
+    d2h = host_out[0].numel() * 4
 
     # ---- accounting
     flops_layer = [ff.ffn_path_flops(d, f, T, k) for k in ks]
@@ -498,7 +531,10 @@ def run_gpu(args, rank: int, world: int) -> None:
                          "32 distinct layers per step); no flush"},
         "e2e": {"value": e2e_ms / L, "unit": "ms/layer", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                "api": "paper_2602_00397_b200.sparse_ffn_layer (x from pinned host f32)"},
+                "api": "paper_2602_00397_b200.sparse_ffn_layer (x from pinned host f32)",
+                "copies": "per step: H2D of its input, D2H of its output, on a copy stream "
+                          "double-buffered against compute (first upload / last readback "
+                          "exposed)", "steps": n_e2e},
         "gpu_launches": launches,
         "effective_tflops": eff_tflops,
         "prefill_ffn_tokens_per_s": prompts * T / (step_ms * 1e-3),
