@@ -15,23 +15,28 @@
 #define FFWD_DOWN_PRODUCERS 8
 #endif
 #define FFWD_PRODUCER_WARPS FFWD_DOWN_PRODUCERS
-// Options (off by default): split rings as in K2 (A = H on its own loader warp, 4-deep;
-// gathered B 5-deep) and CTA pairs (FFWD_DOWN_PAIR: the two CTAs of a cluster run column
-// tiles (j, j+1) of one block and each loads half of its H tile, multicast to both).
-// ncu, 8B/16K: pairs cut K3's L2->SM bytes 6.8% but raise its DRAM reads from 1.64 to
-// 2.0-2.4 GB for every raster group size, and are within noise in the stack.
+#define FFWD_GATHER_ROWS 64  // BK K rows per stage
+// Split rings as in K2 (A = H on its own loader warp, 4-deep; gathered B 5-deep; 224 KiB):
+// on by default (FFWD_DOWN_UNSPLIT: one shared ring, A loaded by producer warp 0).  r1 A/B,
+// two boxes: K3 2-5% faster in the stack (1.12 -> 1.06 and 1.17 -> 1.11 ms/layer), tensor
+// pipe 55.9 -> 59.4% under ncu.
+// Option (off): CTA pairs (FFWD_DOWN_PAIR: the two CTAs of a cluster run column tiles
+// (j, j+1) of one block and each loads half of its H tile, multicast to both).  ncu,
+// 8B/16K: pairs cut K3's L2->SM bytes 6.8% but raise its DRAM reads from 1.64 to 2.0-2.4 GB
+// for every raster group size, and are within noise in the stack.
 #ifdef FFWD_DOWN_PAIR
-#define FFWD_DOWN_SPLIT
 #define FFWD_PAIR_A
 #endif
-#ifdef FFWD_DOWN_SPLIT
+#if !defined(FFWD_DOWN_UNSPLIT) || defined(FFWD_DOWN_PAIR)
 #define FFWD_SPLIT_RING
-#ifndef FFWD_STAGES_A
-#define FFWD_STAGES_A 4
+#ifndef FFWD_DOWN_STAGES_A
+#define FFWD_DOWN_STAGES_A 4
 #endif
-#ifndef FFWD_STAGES_B
-#define FFWD_STAGES_B 5
+#ifndef FFWD_DOWN_STAGES_B
+#define FFWD_DOWN_STAGES_B 5
 #endif
+#define FFWD_STAGES_A FFWD_DOWN_STAGES_A
+#define FFWD_STAGES_B FFWD_DOWN_STAGES_B
 #endif
 #include "gemm_sm100.cuh"
 #include "launch.cuh"

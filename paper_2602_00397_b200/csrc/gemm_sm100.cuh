@@ -66,6 +66,14 @@ constexpr int kABytes = BM * BK * 2;  // 16 KiB
 
 __host__ __device__ constexpr int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
+// rows gathered per stage: the up projection gathers its 256 B-operand rows, the down
+// projection its 64 K rows (FFWD_GATHER_ROWS; smaller row staging leaves K3 room for a
+// co-resident CTA of the overlapped TP completion)
+#ifndef FFWD_GATHER_ROWS
+#define FFWD_GATHER_ROWS 256
+#endif
+constexpr int kGatherRows = FFWD_GATHER_ROWS;
+
 struct Barriers {
   uint64_t full[kStagesB];   // B (and, unsplit, A) landed
   uint64_t empty[kStagesB];
@@ -75,7 +83,7 @@ struct Barriers {
   uint64_t tempty[2];
   uint32_t tmem_base;
   uint32_t pad;
-  alignas(16) int rows[kProducerWarps][256 / kProducerWarps];  // gather row ids (int4 reads)
+  alignas(16) int rows[kProducerWarps][kGatherRows / kProducerWarps];  // gather row ids (int4)
 };
 
 template <int kBBytes>

@@ -27,7 +27,7 @@ struct Bars {
 __global__ void __launch_bounds__(512, 1)
     tma_kernel(const __grid_constant__ CUtensorMap tm_tile, const __grid_constant__ CUtensorMap tm_g,
                const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_a2,
-               const int* __restrict__ rows_all, int n_rowsets, int iters, int stages, int mode,
+               const __grid_constant__ CUtensorMap tm_g2, const int* __restrict__ rows_all, int n_rowsets, int iters, int stages, int mode,
                int kdim, unsigned long long* cycles, const __nv_bfloat16* wptr, int share_a) {
   extern __shared__ uint8_t raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
@@ -35,7 +35,7 @@ __global__ void __launch_bounds__(512, 1)
   __shared__ int srows[256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // barrier arrivals per fill: TMA modes count issuing warps; cp.async modes count threads
-  const int nwarps_issue = (mode == 13 || mode == 14) ? 16 : mode == 12 ? 8 : mode == 10 ? 8 : mode == 11 ? 16 : mode == 7 ? 128 : mode == 8 ? 256 : mode == 9 ? 128 + 2 :
+  const int nwarps_issue = (mode == 13 || mode == 14 || mode == 15) ? 16 : mode == 12 ? 8 : mode == 10 ? 8 : mode == 11 ? 16 : mode == 7 ? 128 : mode == 8 ? 256 : mode == 9 ? 128 + 2 :
                            mode == 5 ? 8 : (mode == 6 ? 16 : (mode >= 2 ? 4 : 1));
   if (threadIdx.x == 0) {
     for (int i = 0; i < kMaxStages; ++i) mbar_init(&bars->full[i], nwarps_issue);
@@ -121,6 +121,23 @@ __global__ void __launch_bounds__(512, 1)
         }
       }
       asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else if (mode == 15) {
+      // mode 14's pattern (64 rows x 4 chunks per stage) from a CHUNK-MAJOR copy of the
+      // matrix ([kdim/64][rows][64]): the 4 chunks of a row are 2 MiB apart, not adjacent
+      const int per = 16 / 16;
+      const int kb2 = (it + blockIdx.x) % (kdim / 256);
+      if (warp < 16 && lane == 0) {
+        mbar_arrive_expect_tx(&bars->full[s], kStageBytes / 16);
+        const int4* rq = reinterpret_cast<const int4*>(srows) + warp * per;
+        for (int q = 0; q < per; ++q) {
+          const int4 r = rq[q];
+          for (int c = 0; c < 4; ++c) {
+            const int cr = (kb2 * 4 + c) * 16384;
+            tma_gather4(&tm_g2, &bars->full[s], dst + ((warp * per + q) * 4 + c) * 512, 0,
+                        cr + r.x, cr + r.y, cr + r.z, cr + r.w, pol);
+          }
+        }
+      }
     } else if (mode == 13 || mode == 14) {
       // 16 warps, same 32 KiB per stage, but each 4-row group fetches `nch` ADJACENT
       // 128 B column chunks back to back (mode 13: 128 rows x 2 chunks, the interleaved
@@ -244,6 +261,12 @@ int main(int argc, char** argv) {
   enc(&g, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims, str, box_g, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
       CU_TENSOR_MAP_SWIZZLE_128B, (CUtensorMapL2promotion)promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   printf("gather promotion %d\n", promo);
+  CUtensorMap g2;  // chunk-major view: [kdim/64 * rows_total] rows of 64 elements
+  cuuint64_t dims2[2] = {64, cuuint64_t(rows_total) * (kdim / 64)};
+  cuuint64_t str2[1] = {128};
+  enc(&g2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, w, dims2, str2, box_g, es,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, (CUtensorMapL2promotion)promo,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   const int n_sets = 148;
   std::vector<int> hrows(n_sets * 256);
   srand(1);
@@ -263,14 +286,14 @@ int main(int argc, char** argv) {
   const size_t smem = 1024 + kMaxStages * kStageBytes + 1024 + kMaxStages * 16384 + sizeof(Bars);
   cudaFuncSetAttribute(tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int iters = 2000;
-  const char* names[15] = {"tile 64x256", "gather4 x64 (1 thread)", "gather4 x64 (4 warps)",
+  const char* names[16] = {"tile 64x256", "gather4 x64 (1 thread)", "gather4 x64 (4 warps)",
                           "gather4 4w preload", "gather4 4w x16 lanes", "gather4 8 warps",
                           "gather4 16 warps", "cp.async 128 thr", "cp.async 256 thr",
-                          "half gather4 + half cp.async", "K2 stage, 8 warps", "K2 stage, 16 warps", "K2 stage 8w A-multicast", "gather4 16w 2 adjacent chunks", "gather4 16w 4 adjacent chunks"};
-  for (int mode = 0; mode < 15; ++mode) {
+                          "half gather4 + half cp.async", "K2 stage, 8 warps", "K2 stage, 16 warps", "K2 stage 8w A-multicast", "gather4 16w 2 adjacent chunks", "gather4 16w 4 adjacent chunks", "gather4 16w 4 chunks, chunk-major"};
+  for (int mode = 0; mode < 16; ++mode) {
     if (mode == 1 || mode == 3 || mode == 4 || mode == 7 || mode == 9) continue;
     for (int stages : {4}) {
-      if (mode != 12) tma_kernel<<<148, 512, smem>>>(tile, g, amap, amap2, drows, n_sets, 50, stages, mode, kdim, dcyc, (const __nv_bfloat16*)w, share);
+      if (mode != 12) tma_kernel<<<148, 512, smem>>>(tile, g, amap, amap2, g2, drows, n_sets, 50, stages, mode, kdim, dcyc, (const __nv_bfloat16*)w, share);
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
@@ -282,10 +305,10 @@ int main(int argc, char** argv) {
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = csz; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
         cfg.attrs = at; cfg.numAttrs = 1;
-        cudaLaunchKernelEx(&cfg, tma_kernel, tile, g, amap, amap2, (const int*)drows, n_sets, iters,
+        cudaLaunchKernelEx(&cfg, tma_kernel, tile, g, amap, amap2, g2, (const int*)drows, n_sets, iters,
                            stages, mode, kdim, dcyc, (const __nv_bfloat16*)w, share);
       } else
-      tma_kernel<<<148, 512, smem>>>(tile, g, amap, amap2, drows, n_sets, iters, stages, mode, kdim, dcyc, (const __nv_bfloat16*)w, share);
+      tma_kernel<<<148, 512, smem>>>(tile, g, amap, amap2, g2, drows, n_sets, iters, stages, mode, kdim, dcyc, (const __nv_bfloat16*)w, share);
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
       float ms;
