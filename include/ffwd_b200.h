@@ -258,7 +258,7 @@ FFWD_API int ffwd_allreduce_residual(const float* const* partials, float* const*
  * overlapped with the down projection: this rank's K3 writes its partial Y into
  * partials[tp_rank] and publishes, per 128-token block, how many column tiles are done
  * (y_done[tp_rank][b] += 1 per tile, system-scope release); a completion kernel on
- * `comm_stream` (comm_ctas CTAs, default 16) starts when this rank's up projection
+ * `comm_stream` (comm_ctas CTAs, default 32) starts when this rank's up projection
  * retires and, block by block in the plan's raster order, waits for y_done[p][b] >=
  * y_epoch * (d / 256) on every rank p and then does ffwd_allreduce_residual's work for
  * its 1/N of the block's rows.  So the reduce-scatter + all-gather of block b over

@@ -750,7 +750,7 @@ int ffwd_ffn_layer_tp_overlap(const void* x_bf16, int T, int d, const void* wgu_
   const unsigned target = y_epoch * static_cast<unsigned>(d / bn_for(d));
   FFWD_CUDA(launch_allreduce_overlap(partials, outs, xnexts, flags, y_done, tp_size, tp_rank,
                                      residual, T, d, epoch, target, b0, nb,
-                                     comm_ctas > 0 ? comm_ctas : 16, cs),
+                                     comm_ctas > 0 ? comm_ctas : 32, cs),
             "allreduce_overlap");
   FFWD_CUDA(cudaEventRecord(ev_done, cs), "event record");
   FFWD_CUDA(cudaStreamWaitEvent(s, ev_done, 0), "stream wait");

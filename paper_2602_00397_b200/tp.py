@@ -131,7 +131,7 @@ def sparse_ffn_layer_tp_overlap(x, packed: PackedLayer, predictor: DevicePredict
                                 partials, outs, flags, y_done, residual: torch.Tensor,
                                 epoch: int, y_epoch: int, xnexts=None,
                                 dense_first_last: bool = True, has_comp: bool = True,
-                                comm_ctas: int = 16, x_pred_f32=None, logits_in=None,
+                                comm_ctas: int = 32, x_pred_f32=None, logits_in=None,
                                 workspace: torch.Tensor | None = None, comm_stream=None):
     """One rank's TP layer with the completion overlapped (``ffwd_ffn_layer_tp_overlap``).
 
@@ -231,7 +231,7 @@ class PeerBuffers:
 
     def layer_overlap(self, x, packed: PackedLayer, predictor: DevicePredictor, k: int,
                       residual: torch.Tensor, dense_first_last: bool = True,
-                      comm_ctas: int = 16, **kw) -> torch.Tensor:
+                      comm_ctas: int = 32, **kw) -> torch.Tensor:
         """This rank's layer with the completion overlapped with its down projection:
         afterwards every rank's ``out`` holds residual + the full FFN output (``xnext``
         its bf16 copy; it must not be the layer input ``x``)."""
