@@ -180,9 +180,50 @@ def _ipc_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_peer_buffers_across_processes(ff):
-    """Two processes on the one GPU: CUDA IPC handle exchange (PeerBuffers) and the fused
-    completion over the mapped peer buffers."""
+def _ipc_overlap_worker(rank, world, port, q):
+    import os
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2602_00397_b200 as ff
+        from paper_2602_00397_b200.tp import PeerBuffers
+        from tests.fixtures import load_case
+        c = load_case("cfg1")
+        lw, pred, comp = c["lw"], c["pred"], ff.CompensatorParams(**c["comp"])
+        xb = torch.from_numpy(c["x"]).cuda().to(torch.bfloat16)
+        T, d = xb.shape
+        k = int(c["k"])
+        dp = ff.DevicePredictor.from_params(ff.PredictorParams(**pred), "cuda")
+        pk = ff.pack_layer(lw["w_gate"], lw["w_up"], lw["w_down"], comp, device="cuda",
+                           tp_rank=rank, tp_size=world)
+        part = ff.sparse_ffn_layer(xb, pk, dp, k).cpu()
+        parts = [None] * world
+        dist.all_gather_object(parts, part)
+        res0 = torch.arange(T * d, dtype=torch.float32).reshape(T, d) * 1e-4
+        want = res0.clone()
+        for p in parts:
+            want = want + p
+        pb = PeerBuffers(T, d, "cuda:0", with_xnext=True)
+        ok = []
+        for _ in range(2):  # counters and flags reused across layers
+            pb.out.copy_(res0)
+            torch.cuda.synchronize()
+            dist.barrier()
+            out = pb.layer_overlap(xb, pk, dp, k, residual=pb.out).clone()
+            torch.cuda.synchronize()
+            dist.barrier()
+            ok.append(bool(torch.equal(out.cpu(), want))
+                      and bool(torch.equal(pb.xnext.cpu(), want.to(torch.bfloat16))))
+        q.put((rank, all(ok)))
+        dist.barrier()
+        pb.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn_two(target):
     import socket
     import torch.multiprocessing as mp
     with socket.socket() as s:
@@ -190,14 +231,28 @@ def test_peer_buffers_across_processes(ff):
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=target, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
         p.join(timeout=240)
     results = sorted(q.get(timeout=5) for _ in range(2))
     assert all(p.exitcode == 0 for p in procs)
-    assert results == [(0, True, True), (1, True, True)]
+    return results
+
+
+def test_peer_buffers_across_processes(ff):
+    """Two processes on the one GPU: CUDA IPC handle exchange (PeerBuffers) and the fused
+    completion over the mapped peer buffers."""
+    assert _spawn_two(_ipc_worker) == [(0, True, True), (1, True, True)]
+
+
+def test_overlapped_layer_across_processes(ff):
+    """Two processes on the one GPU, TP=2 shards of the cfg1 layer: ``layer_overlap`` over
+    CUDA IPC peer buffers (partials, outputs, flags and the per-block tile counters all
+    mapped from the other process) equals residual + the two ranks' partials in rank
+    order, bit for bit, on both ranks and over two layers."""
+    assert _spawn_two(_ipc_overlap_worker) == [(0, True), (1, True)]
 
 
 @pytest.mark.parametrize("collective", ["fused", "overlap"])
