@@ -515,6 +515,35 @@ def run_gpu(args, rank: int, world: int) -> None:
             traffic = json.load(fh).get(args.config, {}).get("up_proj")
     launches = sum(n for _, n in stages.values())
 
+    # per-kernel rooflines: algorithmic FLOPs or bytes per launch / the
+    # event-timed average launch (instrumented run), against the measured peaks
+    def avg_ms(name):
+        ms, n = stages.get(name, (0.0, 0))
+        return ms / n if n else None
+
+    def kroof(bound, work, ms, unit):
+        if not ms:
+            return None
+        peak = peaks["bf16_sus"] if bound == "tensor" else peaks["hbm"]
+        ach = work / (ms * 1e-3) / (1e12 if bound == "tensor" else 1e9)
+        return {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                "avg_launch_ms": ms}
+
+    r_pred = ff.default_reduced_dim(d)
+    dn_flops = sum(n_pred * (2 * 128 * d * k + 2 * 128 * rc * d) + 2 * 2 * 128 * d * f
+                   for k in ks) / L
+    k1_bytes = sum(T * d * 2 + d * r_pred * 4 + r_pred * f * 4 + 2 * n_pred * f * 4
+                   + n_pred * k * 4 for k in ks) / L
+    k1_ms = [avg_ms(s_) for s_ in ("pool", "predictor_w1", "predictor_w2", "topk")]
+    kernels_roofline = {
+        "up_proj": kroof("tensor", up_flops / tp, up_avg_ms, "TFLOP/s"),
+        "down_proj": kroof("tensor", dn_flops / tp, avg_ms("down_proj"), "TFLOP/s"),
+        "predictor+topk (K1: pool, W1, W2, top-k)": kroof(
+            "hbm", k1_bytes, sum(m for m in k1_ms if m) if all(k1_ms) else None, "GB/s"),
+        "ffn_norm (RMSNorm + predictor logits)": kroof(
+            "hbm", T * d * 4 + T * d * 2 + T * 4, avg_ms("ffn_norm"), "GB/s"),
+    }
+
     out = {
         "metric": METRIC, "value": value, "unit": "ms/layer", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
@@ -545,6 +574,10 @@ def run_gpu(args, rank: int, world: int) -> None:
                      "peak_src": f"{peaks['src']} bf16 sustained (burst {peaks['bf16']})",
                      "traffic": traffic},
         "kernels_ms_per_layer": {k_: v[0] / max(1, args.steps * L) for k_, v in stages.items()},
+        "kernels_roofline": kernels_roofline,
+        "kernels_roofline_note": ("K1 bytes per SURVEY 8(d): X bf16 + W1 + W2 + scores + "
+                                  "indices; K1 computes in f64 (exact scores), so it runs "
+                                  "far below the HBM roof by design"),
         "kernels_timing": "CUDA events around each launch, in a second (instrumented) run of the same steps",
         "clocks": clocks,
     }
