@@ -21,7 +21,13 @@ i's compute on a copy stream, double-buffered).  Every input (X 128 MiB, weights
 layer) is larger than L2 and each layer has its own weights, so no L2 flush is
 needed between iterations.
 
-Under torchrun (N > 1): tensor parallel over d_ffn (strided neuron shards,
+Under torchrun (N > 1), by default (`--parallel sp`): the prompt's 128-token
+blocks are split into N contiguous shards, one per GPU, with the weights
+replicated.  The FFN branch is block-local (engine.py:254-310: each block's
+predictor, top-k, FFN and compensator see only that block), so no data-path
+collective exists; only the ranks holding the prompt's first / last block run
+it dense.  Scaling "strong" (one prompt, total work fixed).
+`--parallel tp`: tensor parallel over d_ffn (strided neuron shards,
 replicated predictor, sharded compensator) with one all-reduce of each layer's
 output -- NCCL, or with `--collective fused` the peer-memory kernel that also
 adds the residual (tp.PeerBuffers), or with `--collective overlap` that kernel
@@ -371,14 +377,23 @@ def run_gpu(args, rank: int, world: int) -> None:
     gx = torch.Generator(device=dev)
     gx.manual_seed(99 + (rank if args.parallel == "dp" else 0))
     x0 = torch.randn((T, d), generator=gx, device=dev).to(torch.bfloat16).float()
+    # sp: this rank's contiguous share of the prompt's 128-token blocks; only the ranks
+    # holding the prompt's first / last block run it dense (engine.py:258-262)
+    dfl, blk0, blk1 = True, 0, n_blk
+    if args.parallel == "sp" and world > 1:
+        blk0, blk1, dfl = fl.seq_shard(n_blk, rank, world)
+        x0 = x0[blk0 * 128:min(T, blk1 * 128)].contiguous()
+    T_loc = x0.shape[0]
+    n_dense_loc = int(blk0 == 0) + int(blk1 == n_blk) if dfl != True else min(2, n_blk)  # noqa: E712
+    n_pred_loc = (blk1 - blk0) - n_dense_loc
     res = torch.empty_like(x0)
-    xb = torch.empty((T, d), dtype=torch.bfloat16, device=dev)
+    xb = torch.empty((T_loc, d), dtype=torch.bfloat16, device=dev)
     ybuf = torch.empty_like(x0) if tp > 1 else None
-    ws_bytes = max(fl.layer_workspace_bytes(T, p, dp.r, k, True) for p, dp, k in layers)
+    ws_bytes = max(fl.layer_workspace_bytes(T_loc, p, dp.r, k, dfl) for p, dp, k in layers)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
 
     gain = torch.ones(d, device=dev)            # ffn_norm gains (ones, synthetic.py:41)
-    lg = torch.empty((T,), dtype=torch.float32, device=dev)
+    lg = torch.empty((T_loc,), dtype=torch.float32, device=dev)
     peers = None
     if tp > 1 and args.collective in ("fused", "overlap"):
         # fused completion: partial Y -> peer-memory reduce + residual add (tp.PeerBuffers)
@@ -394,7 +409,7 @@ def run_gpu(args, rank: int, world: int) -> None:
             rmsnorm(res, gain, out=xb, predictor=dp, logits=lg)
             if tp == 1:
                 ff.sparse_ffn_layer(xb, packed, dp, k, out=res, residual=res, logits_in=lg,
-                                    workspace=ws)
+                                    workspace=ws, dense_first_last=dfl)
             elif args.collective == "overlap":
                 peers.layer_overlap(xb, packed, dp, k, residual=res, logits_in=lg,
                                     workspace=ws)
@@ -450,11 +465,11 @@ def run_gpu(args, rank: int, world: int) -> None:
     # from pinned host memory and reads its result back; the copies run on a copy stream,
     # double-buffered, so step i+1's upload and step i's readback overlap step i's compute
     # (the first upload and the last readback are exposed inside the timed region).
-    host_in = torch.empty((T, d), dtype=torch.float32, pin_memory=True)
+    host_in = torch.empty((T_loc, d), dtype=torch.float32, pin_memory=True)
     host_in.copy_(x0.cpu())
     host_out = [torch.empty_like(host_in, pin_memory=True) for _ in range(2)]
-    xd = [torch.empty((T, d), dtype=torch.float32, device=dev) for _ in range(2)]
-    yd = [torch.empty((T, d), dtype=torch.float32, device=dev) for _ in range(2)]
+    xd = [torch.empty((T_loc, d), dtype=torch.float32, device=dev) for _ in range(2)]
+    yd = [torch.empty((T_loc, d), dtype=torch.float32, device=dev) for _ in range(2)]
     copy_s = torch.cuda.Stream(dev)
     ev = {key: [torch.cuda.Event() for _ in range(2)] for key in ("in", "x_free", "y", "out")}
 
@@ -503,8 +518,8 @@ def run_gpu(args, rank: int, world: int) -> None:
     up_ms, up_n = stages["up_proj"]
     dn_ms, dn_n = stages["down_proj"]
     rc = ff.default_comp_dim(d)
-    n_pred = max(0, n_blk - 2)
-    up_flops = sum(n_pred * (4 * 128 * d * k + 2 * 128 * d * rc) + 2 * 4 * 128 * d * f
+    n_pred = n_pred_loc  # this rank's predicted / dense blocks (all of them unless sp)
+    up_flops = sum(n_pred * (4 * 128 * d * k + 2 * 128 * d * rc) + n_dense_loc * 4 * 128 * d * f
                    for k in ks) / L
     up_avg_ms = up_ms / max(1, up_n)
     achieved = up_flops / tp / (up_avg_ms * 1e-3) / 1e12
@@ -530,9 +545,9 @@ def run_gpu(args, rank: int, world: int) -> None:
                 "avg_launch_ms": ms}
 
     r_pred = ff.default_reduced_dim(d)
-    dn_flops = sum(n_pred * (2 * 128 * d * k + 2 * 128 * rc * d) + 2 * 2 * 128 * d * f
+    dn_flops = sum(n_pred * (2 * 128 * d * k + 2 * 128 * rc * d) + n_dense_loc * 2 * 128 * d * f
                    for k in ks) / L
-    k1_bytes = sum(T * d * 2 + d * r_pred * 4 + r_pred * f * 4 + 2 * n_pred * f * 4
+    k1_bytes = sum(T_loc * d * 2 + d * r_pred * 4 + r_pred * f * 4 + 2 * n_pred * f * 4
                    + n_pred * k * 4 for k in ks) / L
     k1_ms = [avg_ms(s_) for s_ in ("pool", "predictor_w1", "predictor_w2", "topk")]
     kernels_roofline = {
@@ -541,7 +556,7 @@ def run_gpu(args, rank: int, world: int) -> None:
         "predictor+topk (K1: pool, W1, W2, top-k)": kroof(
             "hbm", k1_bytes, sum(m for m in k1_ms if m) if all(k1_ms) else None, "GB/s"),
         "ffn_norm (RMSNorm + predictor logits)": kroof(
-            "hbm", T * d * 4 + T * d * 2 + T * 4, avg_ms("ffn_norm"), "GB/s"),
+            "hbm", T_loc * d * 4 + T_loc * d * 2 + T_loc * 4, avg_ms("ffn_norm"), "GB/s"),
     }
 
     out = {
@@ -553,8 +568,8 @@ def run_gpu(args, rank: int, world: int) -> None:
         "config": {"workload": WORKLOAD_NAMES[args.config], "global_batch": 1, "seq_len": T,
                    "layers": L, "keep": keep, "k_per_layer": ks if args.config == "qwen8b"
                    else ks[0], "block": 128, "dense_first_last": True,
-                   "parallelism": f"tp{tp}" if tp > 1 else (f"dp{world}" if world > 1
-                                                            else "single"),
+                   "parallelism": f"tp{tp}" if tp > 1 else (
+                       f"{args.parallel}{world}" if world > 1 else "single"),
                    "collective": args.collective if tp > 1 else None,
                    "l2": "inputs larger than L2 (X 128 MiB, 361 MiB weights per layer, "
                          "32 distinct layers per step); no flush"},
@@ -642,9 +657,11 @@ def main():
     ap.add_argument("--collective", default="nccl", choices=["nccl", "fused", "overlap"],
                     help="TP completion: NCCL all-reduce, the fused peer-memory kernel, or "
                          "that kernel overlapped with the down projection block by block")
-    ap.add_argument("--parallel", default="tp", choices=["tp", "dp"],
-                    help="N>1: tensor parallel over d_ffn (one prompt) or data parallel "
-                         "(one prompt per GPU)")
+    ap.add_argument("--parallel", default="sp", choices=["sp", "tp", "dp"],
+                    help="N>1: sequence parallel (the prompt's 128-token blocks split "
+                         "across GPUs, weights replicated, no collective), tensor parallel "
+                         "over d_ffn (one all-reduce per layer), or data parallel (one "
+                         "prompt per GPU)")
     ap.add_argument("--raster", default="", help="UP,DOWN blocks per L2 raster group (tuning)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

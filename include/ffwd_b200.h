@@ -116,7 +116,9 @@ FFWD_API int ffwd_sparse_ffn(const void* x_bf16, int T, int d, const void* wgu_t
 /*
  * One layer of the FFN branch of the block-wise prefill, all blocks at once.
  * Replaces the engine.py:254-310 FFN branch (mode "predicted") for one layer:
- * dense first/last block when dense_first_last (engine.py:258-262), dense when
+ * dense first/last block when dense_first_last (engine.py:258-262; 1 = the whole
+ * prompt, 2 / 3 = a sequence shard holding only the prompt's first / last block, so
+ * only that one is dense; 0 = none), dense when
  * k >= f_global (engine.py:268), otherwise predictor -> top-k -> sparse FFN ->
  * compensation (has_comp).  The residual add (engine.py:308) stays with the
  * caller unless `residual` is given: then y = residual + FFN(x) (y may alias

@@ -420,8 +420,11 @@ static void layer_split(int T, int k, int f_global, int dense_first_last, int* b
     *begin = 0;
     *count = 0;
   } else if (dense_first_last) {  // engine.py:258-262
-    *begin = 1;
-    *count = n_blk > 2 ? n_blk - 2 : 0;
+    // 1: the whole prompt (first and last block dense); 2 / 3: a sequence shard holding
+    // only the prompt's first / only its last block
+    const int first = dense_first_last != 3 ? 1 : 0, last = dense_first_last != 2 ? 1 : 0;
+    *begin = first;
+    *count = n_blk > first + last ? n_blk - first - last : 0;
   } else {
     *begin = 0;
     *count = n_blk;
@@ -455,6 +458,8 @@ int ffwd_ffn_layer2(const void* x_bf16, int T, int d, const void* wgu_t, const v
   if ((rc = check_gemm_shapes(d, f_local))) return rc;
   if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size)
     return fail(FFWD_ERR_VALIDATION, "bad tensor-parallel rank %d of %d", tp_rank, tp_size);
+  if (dense_first_last < 0 || dense_first_last > 3)
+    return fail(FFWD_ERR_VALIDATION, "dense_first_last must be 0..3, got %d", dense_first_last);
   if (f_local != (f_global - tp_rank + tp_size - 1) / tp_size)
     return fail(FFWD_ERR_VALIDATION, "f_local=%d is not rank %d's strided share of d_ffn=%d",
                 f_local, tp_rank, f_global);
@@ -567,6 +572,8 @@ int ffwd_ffn_layer_mode(const void* x_bf16, int T, int d, const void* wgu_t, con
   if ((rc = check_gemm_shapes(d, f))) return rc;
   if (mode != 1 && mode != 2)
     return fail(FFWD_ERR_VALIDATION, "mode %d: expected 1 (oracle) or 2 (static)", mode);
+  if (dense_first_last != 0 && dense_first_last != 1)
+    return fail(FFWD_ERR_VALIDATION, "ablation modes take dense_first_last 0 or 1");
   if (has_comp && rc_local < 1) return fail(FFWD_ERR_VALIDATION, "compensator width must be >= 1");
   if (workspace_bytes <
       ffwd_ffn_layer_mode_workspace_bytes(T, d, f, rc_local, k, mode, dense_first_last))
@@ -695,6 +702,8 @@ int ffwd_ffn_layer_tp_overlap(const void* x_bf16, int T, int d, const void* wgu_
   if (tp_size < 1 || tp_size > 8 || tp_rank < 0 || tp_rank >= tp_size)
     return fail(FFWD_ERR_VALIDATION, "bad tensor-parallel rank %d of %d (1..8 ranks)", tp_rank,
                 tp_size);
+  if (dense_first_last < 0 || dense_first_last > 3)
+    return fail(FFWD_ERR_VALIDATION, "dense_first_last must be 0..3, got %d", dense_first_last);
   if (f_local != (f_global - tp_rank + tp_size - 1) / tp_size)
     return fail(FFWD_ERR_VALIDATION, "f_local=%d is not rank %d's strided share of d_ffn=%d",
                 f_local, tp_rank, f_global);

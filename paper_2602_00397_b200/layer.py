@@ -164,11 +164,41 @@ def dense_ffn(x, packed: PackedLayer) -> torch.Tensor:
     return run_sparse_ffn(x, packed, None, packed.f_local)
 
 
+_DFL_CODES = {False: 0, True: 1, "first": 2, "last": 3}
+
+
+def dense_first_last_code(v) -> int:
+    """C-ABI code of ``dense_first_last``: a bool for a whole prompt (``engine.py:258-262``),
+    or "first" / "last" for a sequence shard that holds only the prompt's first / last
+    block (only that block runs dense)."""
+    key = v if isinstance(v, str) else bool(v)
+    if key not in _DFL_CODES:
+        raise ValidationError(f"dense_first_last must be a bool, 'first' or 'last', got {v!r}")
+    return _DFL_CODES[key]
+
+
+def seq_shard(n_blk: int, rank: int, world: int):
+    """Sequence parallelism over a prompt's 128-token blocks: rank ``rank`` of ``world``
+    takes the contiguous blocks [b0, b1) and passes ``dense_first_last`` = the returned
+    value, so only the ranks holding the prompt's first / last block run it dense
+    (``engine.py:258-262``).  The FFN branch is block-local, so the shards need no
+    collective."""
+    if not 0 <= rank < world:
+        raise ValidationError(f"bad sequence-parallel rank {rank} of {world}")
+    if n_blk < world:
+        raise ValidationError(f"{n_blk} blocks cannot feed {world} sequence-parallel ranks")
+    b0, b1 = n_blk * rank // world, n_blk * (rank + 1) // world
+    if world == 1:
+        return b0, b1, True
+    return b0, b1, "first" if rank == 0 else ("last" if rank == world - 1 else False)
+
+
 def layer_workspace_bytes(T: int, packed: PackedLayer, r: int, k: int,
-                          dense_first_last: bool) -> int:
+                          dense_first_last) -> int:
     lib = _dev.lib_for(packed.device)
     return int(lib.ffwd_layer_workspace_bytes(T, packed.d, packed.f_global, packed.f_local,
-                                              packed.rc_local, r, k, int(dense_first_last),
+                                              packed.rc_local, r, k,
+                                              dense_first_last_code(dense_first_last),
                                               packed.tp_size))
 
 
@@ -182,7 +212,8 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
     """One layer's FFN branch over every block of x (T, d); returns y (T, d) f32.
 
     Semantics of ``engine.py:254-310`` (mode "predicted"): blocks 0 and n-1 run
-    dense when ``dense_first_last`` (``:258-262``); k >= d_ffn runs every block
+    dense when ``dense_first_last`` (``:258-262``; "first" / "last" for a sequence
+    shard holding only the prompt's first / last block); k >= d_ffn runs every block
     dense with no predictor or compensator (``:268``); otherwise predictor ->
     top-k -> sparse FFN -> + compensator (``:284-300``).  Under tensor
     parallelism y is this rank's partial sum (all-reduce it, see ``tp.py``).
@@ -206,12 +237,11 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
     lib = _dev.lib_for(dev)
     y = out if out is not None else torch.empty((T, d), dtype=torch.float32, device=dev)
     n_blk = -(-T // BLOCK)
+    dfl = dense_first_last_code(dense_first_last)
     if k >= packed.f_global:
         n_pred = 0
-    elif dense_first_last:
-        n_pred = max(0, n_blk - 2)
     else:
-        n_pred = n_blk
+        n_pred = max(0, n_blk - (0 if dfl == 0 else 2 if dfl == 1 else 1))
     idx = None
     if return_indices and n_pred > 0:
         idx = torch.empty((n_pred, k), dtype=torch.int32, device=dev)
@@ -226,7 +256,7 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
     _lib.check(lib.ffwd_ffn_layer2(
         xb.data_ptr(), T, d, packed.wgu_t.data_ptr(), packed.wd.data_ptr(), packed.f_local,
         packed.rc_local, predictor.query.data_ptr(), predictor.w1.data_ptr(),
-        predictor.w2.data_ptr(), predictor.r, predictor.f, k, int(dense_first_last),
+        predictor.w2.data_ptr(), predictor.r, predictor.f, k, dfl,
         int(has_comp and packed.rc_local > 0), packed.tp_rank, packed.tp_size, y.data_ptr(),
         _dev.ptr(residual), _dev.ptr(x_next), _dev.ptr(idx), k if idx is not None else 0,
         _dev.ptr(x_pred_f32), _dev.ptr(logits_in), ws.data_ptr(), ws.numel(),

@@ -26,8 +26,8 @@ import torch.distributed as dist
 from . import _dev, _lib
 from .compensator import CompensatorParams
 from .errors import ValidationError
-from .layer import (BLOCK, PackedLayer, layer_workspace_bytes, pack_layer, shard_comp_cols,
-                    shard_neurons, sparse_ffn_layer)
+from .layer import (BLOCK, PackedLayer, dense_first_last_code, layer_workspace_bytes,
+                    pack_layer, shard_comp_cols, shard_neurons, sparse_ffn_layer)
 from .predictor import DevicePredictor
 
 
@@ -160,7 +160,8 @@ def sparse_ffn_layer_tp_overlap(x, packed: PackedLayer, predictor: DevicePredict
     _lib.check(lib.ffwd_ffn_layer_tp_overlap(
         xb.data_ptr(), T, d, packed.wgu_t.data_ptr(), packed.wd.data_ptr(), packed.f_local,
         packed.rc_local, predictor.query.data_ptr(), predictor.w1.data_ptr(),
-        predictor.w2.data_ptr(), predictor.r, predictor.f, k, int(dense_first_last),
+        predictor.w2.data_ptr(), predictor.r, predictor.f, k,
+        dense_first_last_code(dense_first_last),
         int(has_comp and packed.rc_local > 0), packed.tp_rank, n, None, 0,
         _dev.ptr(x_pred_f32), _dev.ptr(logits_in), _ptr_array(partials), _ptr_array(outs),
         _ptr_array(xnexts) if xnexts is not None else None, _ptr_array(flags),

@@ -274,7 +274,7 @@ def test_bench_tensor_parallel_fused_path_runs(ff, collective):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "2",
            "--config", "1b", "--layers", "2", "--steps", "2", "--warmup", "3",
-           "--collective", collective]
+           "--parallel", "tp", "--collective", collective]
     r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=400)
     assert r.returncode == 0, r.stderr[-3000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]

@@ -71,3 +71,65 @@ def test_tp2_partials_allreduce_to_reference():
     got = out["y"][c["y_rows"]]
     # f64 partial sums of f32 shard results vs the f32 reference: f32 rounding only
     np.testing.assert_allclose(got, c["y"], rtol=0, atol=2e-5)
+
+
+def _sp_worker(rank, world, port, out):
+    """Sequence parallelism: each rank runs the engine's FFN branch (oracle) on its
+    contiguous share of the prompt's blocks (``layer.seq_shard``), dense only where it
+    holds the prompt's first / last block; no collective on the data path -- the shards
+    are gathered here only to check them."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2602_00397_b200 as ff
+        from paper_2602_00397_b200.layer import seq_shard
+        from tests.fixtures import load_case
+        c = load_case("cfg1")
+        lw, pred = c["lw"], c["pred"]
+        comp = ff.CompensatorParams(**c["comp"])
+        n_blk = c["T"] // 128
+        b0, b1, dfl = seq_shard(n_blk, rank, world)
+        y = np.zeros((c["T"], c["x"].shape[1]), dtype=np.float32)
+        for i, j in enumerate(range(b0, b1)):
+            xb = c["x"][j * 128:(j + 1) * 128]
+            dense = (i == 0 and dfl in (True, "first")) or (j == b1 - 1 and dfl in (True, "last"))
+            if dense:
+                y[j * 128:(j + 1) * 128] = orc.dense_ffn(xb, lw["w_gate"], lw["w_up"], lw["w_down"])
+                continue
+            s = orc.predictor_forward(pred["query"], pred["w1"], pred["w2"], xb)
+            g = orc.topk_indices(s, c["k"])
+            y[j * 128:(j + 1) * 128] = (orc.sparse_ffn_forward(xb, lw["w_gate"], lw["w_up"],
+                                                              lw["w_down"], g)
+                                        + orc.compensator_forward(comp.w1, comp.w2, xb))
+        parts = [None] * world
+        dist.all_gather_object(parts, (b0, b1, y[b0 * 128:b1 * 128]))
+        if rank == 0:
+            out["parts"] = parts
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sp2_shards_tile_the_prompt_and_match_reference():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_sp_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    from tests.fixtures import load_case
+    c = load_case("cfg1")
+    parts = sorted(out["parts"], key=lambda p: p[0])
+    n_blk = c["T"] // 128
+    assert parts[0][0] == 0 and parts[-1][1] == n_blk
+    assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))  # contiguous, disjoint
+    y = np.concatenate([p[2] for p in parts])
+    np.testing.assert_allclose(y[c["y_rows"]], c["y"], rtol=0, atol=2e-5)
+
+
+def test_seq_shard_rules():
+    from paper_2602_00397_b200.errors import ValidationError
+    from paper_2602_00397_b200.layer import seq_shard
+    assert seq_shard(128, 0, 1) == (0, 128, True)
+    assert [seq_shard(128, r, 4) for r in range(4)] == [
+        (0, 32, "first"), (32, 64, False), (64, 96, False), (96, 128, "last")]
+    assert [seq_shard(10, r, 3)[:2] for r in range(3)] == [(0, 3), (3, 6), (6, 10)]
+    with pytest.raises(ValidationError):
+        seq_shard(2, 0, 4)
