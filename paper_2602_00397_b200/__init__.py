@@ -19,7 +19,8 @@ from .scheduler import (AttentionMassProfile, SparsityPlan, allocate_budgets, bu
                         dense_plan, load_plan, plan_from_profile, save_plan, uniform_plan)
 from .costmodel import FlopsReport, ffn_path_flops, predict_prefill_flops
 from .layer import (PackedLayer, dense_ffn, ffn_layer_mode, oracle_scores, pack_layer,
-                    run_sparse_ffn, set_raster, shard_comp_cols, shard_neurons, sparse_ffn_layer)
+                    run_sparse_ffn, seq_shard, set_raster, shard_comp_cols, shard_neurons,
+                    sparse_ffn_layer)
 
 __all__ = [name for name in dir() if not name.startswith("_")]
 __version__ = "0.1.0"
