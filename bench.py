@@ -529,6 +529,7 @@ def run_gpu(args, rank: int, world: int) -> None:
         with open(tpath) as fh:
             traffic = json.load(fh).get(args.config, {}).get("up_proj")
     launches = sum(n for _, n in stages.values())
+    w_layer = (3 * f * d + 2 * d * rc) * 2 / tp  # bf16 FFN + compensator weights, this rank
 
     # per-kernel rooflines: algorithmic FLOPs or bytes per launch / the
     # event-timed average launch (instrumented run), against the measured peaks
@@ -571,8 +572,9 @@ def run_gpu(args, rank: int, world: int) -> None:
                    "parallelism": f"tp{tp}" if tp > 1 else (
                        f"{args.parallel}{world}" if world > 1 else "single"),
                    "collective": args.collective if tp > 1 else None,
-                   "l2": "inputs larger than L2 (X 128 MiB, 361 MiB weights per layer, "
-                         "32 distinct layers per step); no flush"},
+                   "l2": (f"inputs larger than L2 (residual stream {T_loc * d * 4 / 2**20:.0f} "
+                          f"MiB f32, {w_layer / 2**20:.0f} MiB bf16 weights per layer, {L} "
+                          "distinct layers per step); no flush")},
         "e2e": {"value": e2e_ms / L, "unit": "ms/layer", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                 "api": "paper_2602_00397_b200.sparse_ffn_layer (x from pinned host f32)",
