@@ -9,7 +9,8 @@ tot = collections.defaultdict(float)
 cnt = collections.Counter()
 for row in r[1:]:
     name = row[ki].split("(")[0].replace("void ", "").replace("ffwd::<unnamed>::", "")
-    if not name.startswith(("pool", "logits", "pooled", "gemm", "topk", "plan", "up_proj", "down_proj")):
+    if not name.startswith(("pool", "logits", "pooled", "gemm", "topk", "plan", "up_proj", "down_proj",
+                            "rmsnorm", "rope", "allreduce", "hidden", "column")):
         name = "other (torch: init / residual copy)"
     scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0}.get(row[ui], 1e-6)
     tot[name] += float(row[vi].replace(",", "")) * scale
