@@ -64,6 +64,22 @@ def test_validation_happens_before_any_launch():
     assert rc == _lib.FFWD_ERR_UNSUPPORTED  # d_model % 64 != 0
     with pytest.raises(_lib.UnsupportedError):
         _lib.check(rc, "ffn_layer")
+    # dense_first_last codes: 0..3 (3 = a sequence shard holding the prompt's last block)
+    args = [None, 256, 512, None, None, 1376, 64, None, None, None, 32, 1376, 688]
+    tail = [1, 0, 1, None, None, None, None, 0, None, None, None, 0, None]
+    assert lib.ffwd_ffn_layer2(*args, 5, *tail) == _lib.FFWD_ERR_VALIDATION
+    assert b"dense_first_last" in lib.ffwd_last_error()
+    # the overlapped TP layer rejects missing peer buffers before touching the device
+    rc = lib.ffwd_ffn_layer_tp_overlap(None, 256, 512, None, None, 688, 32, None, None, None,
+                                       32, 1376, 688, 1, 1, 0, 2, None, 0, None, None, None,
+                                       None, None, None, None, None, 1, 1, 0, None, 0, None,
+                                       None)
+    assert rc == _lib.FFWD_ERR_VALIDATION and b"pointers" in lib.ffwd_last_error()
+    rc = lib.ffwd_ffn_layer_tp_overlap(None, 256, 512, None, None, 688, 32, None, None, None,
+                                       32, 1376, 688, 1, 1, 0, 9, None, 0, None, None, None,
+                                       None, None, None, None, None, 1, 1, 0, None, 0, None,
+                                       None)
+    assert rc == _lib.FFWD_ERR_VALIDATION and b"1..8 ranks" in lib.ffwd_last_error()
 
 
 @pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU path")
