@@ -365,8 +365,9 @@ def run_gpu(args, rank: int, world: int) -> None:
         fl.set_raster(*(int(v) for v in args.raster.split(",")))
     peaks = load_peaks()
     d, f, L, T, keep = CONFIGS[args.config]
-    if args.layers:
-        L = args.layers
+    if args.layers or args.tokens:
+        L = args.layers or L
+        T = args.tokens or T
         CONFIGS[args.config] = (d, f, L, T, keep)
     # tp: tensor parallel over d_ffn (one prompt, NCCL all-reduce per layer);
     # dp: every rank runs the whole stack on its own prompt (independent prompts, no
@@ -653,6 +654,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="8b", choices=sorted(CONFIGS))
     ap.add_argument("--layers", type=int, default=0, help="override layer count (debug)")
+    ap.add_argument("--tokens", type=int, default=0, help="override prompt length (debug)")
     ap.add_argument("--skip-dense", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-ttft", action="store_true")
