@@ -425,7 +425,10 @@ def run_gpu(args, rank: int, world: int) -> None:
 
     def barrier():
         if world > 1:
-            torch.distributed.barrier()
+            if BACKEND == "nccl":
+                torch.distributed.barrier(device_ids=[dev.index])
+            else:
+                torch.distributed.barrier()
 
     def timed(fn, steps):
         barrier()
@@ -675,7 +678,11 @@ def main():
         return
     if world > 1:
         torch.cuda.set_device(local_device())
-        torch.distributed.init_process_group(BACKEND)
+        if BACKEND == "nccl":  # bind the rank's GPU (barriers and collectives use it)
+            torch.distributed.init_process_group(
+                "nccl", device_id=torch.device("cuda", local_device()))
+        else:
+            torch.distributed.init_process_group(BACKEND)
     try:
         run_gpu(args, rank, world)
     finally:
