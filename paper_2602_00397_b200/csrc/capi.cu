@@ -723,7 +723,12 @@ int ffwd_ffn_layer_tp_overlap(const void* x_bf16, int T, int d, const void* wgu_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaStream_t cs = static_cast<cudaStream_t>(comm_stream);
   if (cs == s) return fail(FFWD_ERR_VALIDATION, "the completion needs its own stream");
-  static thread_local cudaEvent_t ev_up = nullptr, ev_done = nullptr;
+  // events belong to a device: one pair per (thread, device)
+  static thread_local cudaEvent_t evs[64][2] = {};
+  int dev = 0;
+  FFWD_CUDA(cudaGetDevice(&dev), "cudaGetDevice");
+  cudaEvent_t& ev_up = evs[dev & 63][0];
+  cudaEvent_t& ev_done = evs[dev & 63][1];
   if (!ev_up) {
     FFWD_CUDA(cudaEventCreateWithFlags(&ev_up, cudaEventDisableTiming), "event create");
     FFWD_CUDA(cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming), "event create");

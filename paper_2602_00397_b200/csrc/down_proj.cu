@@ -314,13 +314,9 @@ cudaError_t launch_bn(const GemmArgs& a, cudaStream_t s) {
   if (encode_tmap_2d_bf16(&twt, a.wd, a.d, a.wd_rows, 64, BK) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   constexpr size_t smem = smem_bytes<BK * BN * 2>();
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(down_proj_kernel<BN>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = ensure_smem_limit(down_proj_kernel<BN>, smem, attr); e != cudaSuccess)
+    return e;
   int grid = a.num_sms < a.down_cap ? a.num_sms : a.down_cap;
   if constexpr (kPairA) {
     grid &= ~1;  // whole CTA pairs; the plan pads the tile table to pairs

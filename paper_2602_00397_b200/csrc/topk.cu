@@ -204,14 +204,10 @@ cudaError_t launch_topk(const float* scores, int n_rows, int f, int k, int tp_ra
   if (n_rows <= 0) return cudaSuccess;
   const size_t smem = static_cast<size_t>(f) * sizeof(uint32_t);
   if (smem <= kTopkMaxSmem) {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(topk_kernel<true>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           static_cast<int>(kTopkMaxSmem));
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
+    static std::atomic<uint64_t> attr{0};
+    if (cudaError_t e = ensure_smem_limit(topk_kernel<true>, kTopkMaxSmem, attr);
+        e != cudaSuccess)
+      return e;
     return launch_k(topk_kernel<true>, dim3(n_rows), dim3(kTopkThreads), smem, s, 1, scores, f,
                     k, tp_rank, tp_size, idx_global, ld_global, idx_local, ld_local, counts);
   } else {

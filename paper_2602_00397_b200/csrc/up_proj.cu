@@ -260,13 +260,8 @@ cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s) {
   if (encode_tmap_2d_bf16(&twt, a.wgu_t, a.d, a.wgu_rows, BK, 128) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   constexpr size_t smem = smem_bytes<kBBytes>();
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(up_proj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = ensure_smem_limit(up_proj_kernel, smem, attr); e != cudaSuccess) return e;
   int grid = a.num_sms < a.up_cap ? a.num_sms : a.up_cap;
   if constexpr (kPairA) {
     grid &= ~1;  // whole CTA pairs; the plan pads the tile table to pairs
