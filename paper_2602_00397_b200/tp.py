@@ -201,6 +201,7 @@ class PeerBuffers:
         dist.all_gather_object(allh, mine, group=group)
         self._opened = []
         self.peer = {"partial": [], "out": [], "xnext": [], "flags": [], "y_done": []}
+        bases: dict = {}  # one mapping per peer allocation (tensors may share a segment)
         for p in range(self.world):
             for key, t, hv in zip(("partial", "out", "xnext", "flags", "y_done"),
                                   (self.partial, self.out, self.xnext, self.flags, self.y_done),
@@ -210,10 +211,12 @@ class PeerBuffers:
                 if p == self.rank:
                     self.peer[key].append(t.data_ptr())
                     continue
-                base = ctypes.c_void_p()
-                _lib.check(lib.ffwd_ipc_open(hv[0], ctypes.byref(base)), "ipc open")
-                self._opened.append(base.value)
-                self.peer[key].append(base.value + hv[1])
+                if (p, hv[0]) not in bases:
+                    base = ctypes.c_void_p()
+                    _lib.check(lib.ffwd_ipc_open(hv[0], ctypes.byref(base)), "ipc open")
+                    self._opened.append(base.value)
+                    bases[(p, hv[0])] = base.value
+                self.peer[key].append(bases[(p, hv[0])] + hv[1])
         self.epoch = 0
         self.y_epoch = 0
         self.comm_stream = torch.cuda.Stream(dev)
