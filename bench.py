@@ -137,7 +137,7 @@ class ClockSampler:
     def summary(self) -> dict:
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in self.rows:
             try:
@@ -145,12 +145,17 @@ class ClockSampler:
                 mx = float(r[2])
             except (ValueError, IndexError):
                 continue
+            try:
+                pw.append(float(r[3]))
+            except (ValueError, IndexError):
+                pass
             for nm, v in zip(names, r[5:9]):
                 if v.strip().lower() == "active":
                     reasons.add(nm)
         loaded = [v for v in sm if v > 0.5 * (mx or 1)] or sm
         return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w": statistics.median(pw) if pw else None}
 
 
 # ------------------------------------------------------------------ model
