@@ -333,6 +333,105 @@ __global__ void __launch_bounds__(GTHREADS)
       }
 }
 
+// The scores GEMM (W2: M = predicted blocks <= 128, K = r, N = d_ffn) with A resident:
+// each persistent CTA loads h (M x K f32) into shared memory once and streams W2 in
+// 16-column tiles, instead of re-reading all of h for every 16 columns.  RG row groups of
+// 32 rows (RG = 1 / 2 for M <= 32 / 64) so small M does not pad to 128 rows;
+// the 4 warps split as RG row groups x 4/RG column sub-tiles.  Every output element is
+// accumulated exactly as in gemm_f64_kernel (same DMMA fragments, same k order), so the
+// scores are bit-identical to it.
+template <int RG>
+__global__ void __launch_bounds__(GTHREADS)
+    gemm_f64_resident_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                             float* __restrict__ C, int M, int K, int N, int relu) {
+  constexpr int CS = 4 / RG;   // 16-column sub-tiles per iteration
+  constexpr int CW = 16 * CS;  // columns per iteration
+  constexpr int BP = CW + 8;
+  extern __shared__ __align__(16) float smf[];
+  const int AP = K + 4;
+  float* As = smf;                    // [32 RG][AP]
+  float* Bs = smf + 32 * RG * AP;     // [2][GBK][BP]
+  pdl_wait();
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int rg = warp % RG, cs = warp / RG;
+  for (int e = threadIdx.x; e < 32 * RG * (K / 4); e += GTHREADS) {
+    const int r = e / (K / 4), c = (e % (K / 4)) * 4;
+    float* dst = As + r * AP + c;
+    if (r < M) {
+      cp_async16(dst, A + static_cast<size_t>(r) * K + c);
+    } else {
+      dst[0] = dst[1] = dst[2] = dst[3] = 0.f;
+    }
+  }
+  cp_async_commit();
+  const int n_tiles = (N + CW - 1) / CW;
+  const int nch = K / GBK;
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const int n0 = t * CW;
+    auto load_b = [&](int buf, int k0) {
+      for (int e = threadIdx.x; e < GBK * (CW / 4); e += GTHREADS) {
+        const int r = e / (CW / 4), c = (e % (CW / 4)) * 4;
+        const int gk = k0 + r, gn = n0 + c;
+        float* dst = Bs + buf * GBK * BP + r * BP + c;
+        const float* src = B + static_cast<size_t>(gk) * N + gn;
+        if (gn + 3 < N) {
+          cp_async16(dst, src);
+        } else {
+          for (int u = 0; u < 4; ++u) dst[u] = gn + u < N ? __ldg(src + u) : 0.f;
+        }
+      }
+      cp_async_commit();
+    };
+    double acc[4][2][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    load_b(0, 0);
+    for (int ch = 0; ch < nch; ++ch) {
+      const int buf = ch & 1;
+      if (ch + 1 < nch) {
+        load_b(buf ^ 1, (ch + 1) * GBK);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const float* bs = Bs + buf * GBK * BP;
+      const int k0 = ch * GBK;
+#pragma unroll
+      for (int ks = 0; ks < GBK / 4; ++ks) {
+        double a[4], bb[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          a[i] = static_cast<double>(As[(32 * rg + 8 * i + fr) * AP + k0 + 4 * ks + fc]);
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+          bb[j] = static_cast<double>(bs[(4 * ks + fc) * BP + 16 * cs + 8 * j + fr]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) dmma(acc[i][j], a[i], bb[j]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gm = 32 * rg + 8 * i + fr, gn = n0 + 16 * cs + 8 * j + 2 * fc + h;
+          if (gm >= M || gn >= N) continue;
+          float f = static_cast<float>(acc[i][j][h]);
+          if (relu) f = fmaxf(f, 0.0f);
+          C[static_cast<size_t>(gm) * N + gn] = f;
+        }
+  }
+}
+
 __global__ void gemm_reduce_kernel(const double* __restrict__ partial, float* __restrict__ C,
                                    int MN, int splits, int relu) {
   pdl_wait();
@@ -399,6 +498,17 @@ cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begi
   return cudaGetLastError();
 }
 
+template <int RG>
+cudaError_t launch_resident(const float* A, const float* B, float* C, int M, int K, int N,
+                            bool relu, size_t smem, int grid, cudaStream_t s) {
+  static std::atomic<uint64_t> attr{0};  // one per instantiation: each kernel needs its own
+  if (cudaError_t e = ensure_smem_limit(gemm_f64_resident_kernel<RG>, smem, attr);
+      e != cudaSuccess)
+    return e;
+  return launch_k(gemm_f64_resident_kernel<RG>, dim3(grid), dim3(GTHREADS), smem, s, 1, A, B, C,
+                  M, K, N, relu ? 1 : 0);
+}
+
 size_t gemm_f64acc_partial_bytes(int M, int K, int N) {
   const int sp = gemm_splits(M, K, N);
   return sp > 1 ? static_cast<size_t>(sp) * M * N * sizeof(double) : 0;
@@ -412,6 +522,24 @@ cudaError_t launch_gemm_f64acc(const float* A, const float* B, float* C, int M, 
   const int z = (K + kper - 1) / kper;
   // Wide outputs (the W2 scores GEMM) take 16-column tiles: twice the CTAs, so more
   // warps per SM keep the DMMA pipe busy.
+  // h resident for up to 64 rows (a sequence shard's or a short prompt's blocks); at 128
+  // rows the resident tile leaves one 4-warp CTA per SM and runs slower (83 vs 54 us at
+  // 8B/16K), so full prompts keep the 16-column tiles below.
+  if (z == 1 && N >= 16 * 4 * 148 && M <= 64 && K % GBK == 0 && N % 4 == 0) {
+    const int rg = M > 32 ? 2 : 1;
+    const size_t smem = (static_cast<size_t>(32 * rg) * (K + 4) +
+                         2 * GBK * (16 * (4 / rg) + 8)) * sizeof(float);
+    if (smem <= 200 * 1024) {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      const int per_sm = std::max(1, static_cast<int>((220 * 1024) / (smem + 1024)));
+      const int tiles = (N + 16 * (4 / rg) - 1) / (16 * (4 / rg));
+      const int grid = std::min(tiles, sms * per_sm);
+      return rg == 2 ? launch_resident<2>(A, B, C, M, K, N, relu, smem, grid, s)
+                     : launch_resident<1>(A, B, C, M, K, N, relu, smem, grid, s);
+    }
+  }
   if (z == 1 && N >= 16 * 4 * 148) {
     const dim3 g16((N + 15) / 16, (M + GBM - 1) / GBM, 1);
     return launch_k(gemm_f64_kernel<16>, g16, dim3(GTHREADS), 0, s, 1, A, B, C,

@@ -305,3 +305,27 @@ def test_layer_edge_shapes_vs_oracle(ff, d, f, T, k, dfl):
         for row, j in enumerate(sorted(masks)):
             np.testing.assert_array_equal(got[row], masks[j])
     assert_close(y.cpu().numpy(), want, f"d{d} f{f} T{T} k{k}")
+
+
+def test_scores_gemm_paths_agree_bit_exactly(ff):
+    """The scores GEMM (predictor.py:80) runs on the h-resident kernel for <= 64 predicted
+    blocks and on 16-column tiles above: the same block gives bit-identical scores either
+    way, and both match the oracle bit for bit (8B predictor shape)."""
+    from oracle import ffwd_oracle as orc
+    d, r, f = 4096, 256, 14336
+    rng = np.random.default_rng(11)
+    q = (rng.standard_normal((1, d)) * 0.02).astype(np.float32)
+    w1 = (rng.standard_normal((d, r)) * 0.02).astype(np.float32)
+    w2 = (rng.standard_normal((r, f)) * 0.02).astype(np.float32)
+    dp = ff.DevicePredictor(query=torch.from_numpy(q[0]).cuda(), w1=torch.from_numpy(w1).cuda(),
+                            w2=torch.from_numpy(w2).cuda())
+    x = torch.randn((126 * 128, d), device="cuda").to(torch.bfloat16).float()
+    from paper_2602_00397_b200.predictor import predictor_scores
+    full = predictor_scores(dp, x)                       # 126 blocks: tiled kernel
+    for n in (14, 40, 62):                               # resident kernel, 1 and 2 row groups
+        part = predictor_scores(dp, x[:n * 128])
+        assert torch.equal(part, full[:n]), f"{n} blocks: scores differ from the tiled path"
+    xs = x.cpu().numpy()
+    for b in (0, 13, 61, 125):
+        want = orc.predictor_forward(q, w1, w2, xs[b * 128:(b + 1) * 128])
+        assert np.array_equal(full[b].cpu().numpy(), want), f"block {b} differs from the oracle"
