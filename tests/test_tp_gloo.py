@@ -133,3 +133,8 @@ def test_seq_shard_rules():
     assert [seq_shard(10, r, 3)[:2] for r in range(3)] == [(0, 3), (3, 6), (6, 10)]
     with pytest.raises(ValidationError):
         seq_shard(2, 0, 4)
+    from paper_2602_00397_b200.layer import dense_first_last_code
+    assert [dense_first_last_code(v) for v in (False, True, "first", "last")] == [0, 1, 2, 3]
+    assert dense_first_last_code(1) == 1 and dense_first_last_code(0) == 0
+    with pytest.raises(ValidationError):
+        dense_first_last_code("middle")
