@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
   const int need_eq = remaining;  // how many keys == thr to keep (lowest index first)
 
   // -- compaction in index order: contiguous chunk per thread
+  const bool tp1 = tp_size == 1;
   const int per = (f + kTopkThreads - 1) / kTopkThreads;
   const int lo = min(f, tid * per), hi = min(f, lo + per);
   int eq = 0;
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
       }
       if (keep) {
         ++kept;
-        kept_loc += (i % tp_size) == tp_rank;
+        kept_loc += tp1 || (i % tp_size) == tp_rank;
       }
     }
   }
@@ -187,8 +188,9 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
     if (!keep) continue;
     if (idx_global) idx_global[static_cast<size_t>(blockIdx.x) * ld_global + p] = i;
     ++p;
-    if ((i % tp_size) == tp_rank) {
-      if (idx_local) idx_local[static_cast<size_t>(blockIdx.x) * ld_local + pl] = i / tp_size;
+    if (tp1 || (i % tp_size) == tp_rank) {  // tp1: skip the integer divisions
+      if (idx_local)
+        idx_local[static_cast<size_t>(blockIdx.x) * ld_local + pl] = tp1 ? i : i / tp_size;
       ++pl;
     }
   }
