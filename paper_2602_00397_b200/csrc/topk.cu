@@ -89,17 +89,24 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
     else return rank_key(__ldg(s + i));
   };
   if constexpr (kCached) {
+    // the first pass's histogram (top 12 bits, every key counts) is built while staging
+    for (int i = tid; i < kBins; i += kTopkThreads) hist[i] = 0;
+    __syncthreads();
+    auto stage = [&](int i, uint32_t key) {
+      s_keys[i] = key;
+      atomicAdd(&hist[key >> digit_shift(0)], 1);
+    };
     if ((f & 3) == 0) {
       const float4* s4 = reinterpret_cast<const float4*>(s);
       for (int i = tid; i < f / 4; i += kTopkThreads) {
         const float4 v = __ldg(s4 + i);
-        s_keys[4 * i] = rank_key(v.x);
-        s_keys[4 * i + 1] = rank_key(v.y);
-        s_keys[4 * i + 2] = rank_key(v.z);
-        s_keys[4 * i + 3] = rank_key(v.w);
+        stage(4 * i, rank_key(v.x));
+        stage(4 * i + 1, rank_key(v.y));
+        stage(4 * i + 2, rank_key(v.z));
+        stage(4 * i + 3, rank_key(v.w));
       }
     } else {
-      for (int i = tid; i < f; i += kTopkThreads) s_keys[i] = rank_key(__ldg(s + i));
+      for (int i = tid; i < f; i += kTopkThreads) stage(i, rank_key(__ldg(s + i)));
     }
   }
 
@@ -109,11 +116,13 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
   for (int pass = 0; pass < 3; ++pass) {
     const int shift = digit_shift(pass);
     const int nb = 1 << digit_bits(pass);
-    for (int i = tid; i < nb; i += kTopkThreads) hist[i] = 0;
-    __syncthreads();
-    for (int i = tid; i < f; i += kTopkThreads) {
-      const uint32_t key = key_at(i);
-      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & (nb - 1)], 1);
+    if (!kCached || pass > 0) {  // cached: pass 0's histogram came with the staging
+      for (int i = tid; i < nb; i += kTopkThreads) hist[i] = 0;
+      __syncthreads();
+      for (int i = tid; i < f; i += kTopkThreads) {
+        const uint32_t key = key_at(i);
+        if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & (nb - 1)], 1);
+      }
     }
     __syncthreads();
     // thread t owns bins [nb-1-B t-(B-1), nb-1-B t] (descending); block scan finds the
