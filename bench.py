@@ -108,13 +108,14 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.rows: list[list[str]] = []
+        self.times: list[float] = []  # arrival time of each row
         self.proc = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -125,6 +126,7 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([c.strip() for c in line.split(",")])
+            self.times.append(time.monotonic())
 
     def __exit__(self, *exc):
         if self.proc is not None:
@@ -134,12 +136,21 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
-    def summary(self) -> dict:
-        if not self.rows:
+    def summary(self, t0: float | None = None, t1: float | None = None) -> dict:
+        """Rows that arrived inside [t0, t1 + 0.3 s] (the timed region; a row arrives shortly
+        after its sample); a region shorter than the sampling period gets the first row
+        after t0, flagged as "nearest"."""
+        rows, note = self.rows, None
+        if t0 is not None and t1 is not None:
+            rows = [r for r, t in zip(self.rows, self.times) if t0 <= t <= t1 + 0.3]
+            if not rows:
+                after = [r for r, t in zip(self.rows, self.times) if t >= t0]
+                rows, note = after[:1], "nearest sample after a timed region shorter than the sampling period"
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "power_w": None}
         sm, mx, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+        for r in rows:
             try:
                 sm.append(float(r[1]))
                 mx = float(r[2])
@@ -153,9 +164,12 @@ class ClockSampler:
                 if v.strip().lower() == "active":
                     reasons.add(nm)
         loaded = [v for v in sm if v > 0.5 * (mx or 1)] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm),
-                "power_w": statistics.median(pw) if pw else None}
+        out = {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": mx,
+               "reasons": sorted(reasons), "samples": len(sm),
+               "power_w": statistics.median(pw) if pw else None}
+        if note:
+            out["note"] = note
+        return out
 
 
 # ------------------------------------------------------------------ model
@@ -452,17 +466,22 @@ def run_gpu(args, rank: int, world: int) -> None:
             ms = float(t.item())
         return ms
 
-    # ---- warm-up, then the timed region (kernel event timing on)
-    for _ in range(args.warmup):
-        stack(x0)
-    torch.cuda.synchronize(dev)
-    # the headline: uninstrumented (per-launch events would sit between the kernels and
-    # defeat the programmatic-dependent-launch overlap)
+    # ---- warm-up, then the timed region.  The clock sampler starts before the warm-up so
+    # nvidia-smi is already sampling when the timed region begins; only rows that arrive
+    # inside the timed region are kept.
     with ClockSampler(dev.index) as clk:
+        for _ in range(args.warmup):
+            stack(x0)
+        torch.cuda.synchronize(dev)
+        # the headline: uninstrumented (per-launch events would sit between the kernels and
+        # defeat the programmatic-dependent-launch overlap)
+        t_on = time.monotonic()
         step_ms = timed(lambda: stack(x0), args.steps)
+        t_off = time.monotonic()
+        time.sleep(0.35)  # let the rows sampled inside the region arrive
     if not bool(torch.isfinite(res).all()):
         raise RuntimeError("non-finite residual stream after the FFN stack")
-    clocks = clk.summary()
+    clocks = clk.summary(t_on, t_off)
     # per-kernel breakdown and launch counts: a second, instrumented run of the same steps
     fl.timing_enable(True)
     fl.timing_read()
