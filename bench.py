@@ -77,6 +77,27 @@ WORKLOAD_NAMES = {
 }
 
 
+def workload_config(args, T: int, L: int, ks, world: int) -> dict:
+    """The workload both arms report (identical dicts: the driver compares them)."""
+    d, f, _, _, keep = CONFIGS[args.config]
+    par = args.parallel if world > 1 else "single"
+    return {"workload": WORKLOAD_NAMES[args.config], "global_batch": 1 if par != "dp" else world,
+            "seq_len": T, "layers": L, "keep": keep,
+            "k_per_layer": list(ks) if args.config == "qwen8b" else ks[0], "block": 128,
+            "dense_first_last": True, "parallelism": par if par == "single" else f"{par}{world}"}
+
+
+def config_ks(cfg_name: str) -> list:
+    """Per-layer k: budget_to_k(keep) everywhere, or the Qwen3 layer-wise schedule
+    (a seeded importance profile through Algorithm 1, scheduler.py:66-98)."""
+    import paper_2602_00397_b200 as ff  # host-side scheduler (scheduler.py mirror)
+    d, f, L, T, keep = CONFIGS[cfg_name]
+    if cfg_name == "qwen8b":
+        s = np.random.default_rng(1234).random(L) + 0.25
+        return [int(k) for k in ff.budgets_to_topk(ff.allocate_budgets(s, keep), f)]
+    return [ff.budget_to_k(keep, f)] * L
+
+
 def load_peaks() -> dict:
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -177,11 +198,7 @@ def make_layers(cfg_name: str, dev, tp_rank: int, tp_size: int, seed: int = 1234
     """Random-init packed layers (normal x 0.02) for this rank + per-layer k."""
     import paper_2602_00397_b200 as ff
     d, f, L, T, keep = CONFIGS[cfg_name]
-    if cfg_name == "qwen8b":
-        s = np.random.default_rng(seed).random(L) + 0.25  # synthetic importance profile
-        ks = ff.budgets_to_topk(ff.allocate_budgets(s, keep), f)
-    else:
-        ks = [ff.budget_to_k(keep, f)] * L
+    ks = config_ks(cfg_name)
     r, rc = ff.default_reduced_dim(d), ff.default_comp_dim(d)
     layers = []
     g = torch.Generator(device=dev)
@@ -280,6 +297,12 @@ def cores() -> int:
 
 
 def run_reference(args, rank: int, world: int) -> None:
+    """The reference's own CPU implementation (baseline/_ref, unmodified) on the host cores.
+
+    Each step is a bounded sample of the workload: one dense and one predicted 128-token
+    block of one layer through the reference's per-block FFN branch (engine.py:254-310).
+    `ms_per_step` is the measured wall time of that sample; `value` extrapolates it to a
+    whole layer (2 dense + n-2 predicted blocks), as the `extrapolation` key states."""
     if rank != 0:
         return
     impl = "reference"
@@ -289,21 +312,34 @@ def run_reference(args, rank: int, world: int) -> None:
     except ImportError:
         impl = "port"
     d, f, L, T, keep = CONFIGS[args.config]
-    step_ms = []
+    if args.layers or args.tokens:
+        L, T = args.layers or L, args.tokens or T
+        CONFIGS[args.config] = (d, f, L, T, keep)
+    layer_ms, wall_ms = [], []
     for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
         ms, info = cpu_sample(args.config, impl, n_sparse=1, seed=1234 + i)
+        wall = (time.perf_counter() - t0) * 1e3
         if i >= args.warmup:
-            step_ms.append(ms)
-    v = float(np.median(step_ms))
-    sample = (f"per step: 1 dense + 1 predicted 128-token block of one layer, extrapolated to "
-              f"{2 if T > 256 else 1} dense + {info['n_blocks'] - 2} predicted blocks")
+            layer_ms.append(ms)
+            wall_ms.append(wall)
+    v = float(np.median(layer_ms))
+    n_blk = info["n_blocks"]
+    n_dense = min(2, n_blk)
+    sample = (f"per step: 1 dense + 1 predicted 128-token block of one layer (engine.py:254-310 "
+              f"FFN branch), extrapolated to {n_dense} dense + {n_blk - n_dense} predicted blocks")
     out = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "ms/layer",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": float(np.mean(wall_ms)),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32/f64",
-        "data": "synthetic (random-init weights, N(0,1) inputs)",
-        "config": {"workload": WORKLOAD_NAMES[args.config], "global_batch": 1, "seq_len": T,
-                   "parallelism": "cpu"},
+        "data": "synthetic (random-init normal*0.02 weights, N(0,1) hidden states)",
+        "config": workload_config(args, T, L, config_ks(args.config), world),
+        "extrapolation": {"measured": "1 dense + 1 predicted block per step",
+                          "t_dense_block_ms": 1e3 * info["t_dense_block_s"],
+                          "t_predicted_block_ms": 1e3 * info["t_sparse_block_s"],
+                          "layer_ms": f"{n_dense} x t_dense + {n_blk - n_dense} x t_predicted",
+                          "ms_per_step_is": "measured wall time of one step's sample"},
         "cpu_baseline": {"value": v, "unit": "ms/layer", "cores": cores(),
                          "kind": "reference" if impl == "reference" else "port",
                          "sample": sample},
@@ -482,6 +518,27 @@ def run_gpu(args, rank: int, world: int) -> None:
     if not bool(torch.isfinite(res).all()):
         raise RuntimeError("non-finite residual stream after the FFN stack")
     clocks = clk.summary(t_on, t_off)
+    # the reference-exact predictor input (engine.py:267,286): the predictor pools the f32
+    # RMSNorm output instead of its bf16 rounding (norm writes both; fused f32 logits)
+    f32_variant = None
+    if tp == 1 and not args.skip_f32_pred:
+        x32 = torch.empty((T_loc, d), dtype=torch.float32, device=dev)
+
+        def stack_f32(x_src: torch.Tensor):
+            res.copy_(x_src)
+            for packed, dp, k in layers:
+                rmsnorm(res, gain, out=xb, out_f32=True, out32=x32, predictor=dp, logits=lg,
+                        logits_from_f32=True)
+                ff.sparse_ffn_layer(xb, packed, dp, k, out=res, residual=res, logits_in=lg,
+                                    x_pred_f32=x32, workspace=ws, dense_first_last=dfl)
+
+        stack_f32(x0)
+        f32_ms = timed(lambda: stack_f32(x0), max(1, args.steps // 2))
+        f32_variant = {"ms_per_layer": f32_ms / L, "vs_bf16_predictor_input": f32_ms / step_ms,
+                       "what": "predictor pools the f32 RMSNorm output (x_pred_f32, f32 fused "
+                               "logits): the reference's own predictor input; the headline's "
+                               "predictor pools the bf16 FFN operand"}
+        del x32
     # per-kernel breakdown and launch counts: a second, instrumented run of the same steps
     fl.timing_enable(True)
     fl.timing_read()
@@ -594,15 +651,11 @@ def run_gpu(args, rank: int, world: int) -> None:
         "higher_is_better": False, "scaling": "weak" if args.parallel == "dp" and world > 1
         else "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init normal*0.02 weights, N(0,1) bf16 hidden states)",
-        "config": {"workload": WORKLOAD_NAMES[args.config], "global_batch": 1, "seq_len": T,
-                   "layers": L, "keep": keep, "k_per_layer": ks if args.config == "qwen8b"
-                   else ks[0], "block": 128, "dense_first_last": True,
-                   "parallelism": f"tp{tp}" if tp > 1 else (
-                       f"{args.parallel}{world}" if world > 1 else "single"),
-                   "collective": args.collective if tp > 1 else None,
-                   "l2": (f"inputs larger than L2 (residual stream {T_loc * d * 4 / 2**20:.0f} "
-                          f"MiB f32, {w_layer / 2**20:.0f} MiB bf16 weights per layer, {L} "
-                          "distinct layers per step); no flush")},
+        "config": workload_config(args, T, L, ks, world),
+        "collective": args.collective if tp > 1 else None,
+        "l2": (f"inputs larger than L2 (residual stream {T_loc * d * 4 / 2**20:.0f} MiB f32, "
+               f"{w_layer / 2**20:.0f} MiB bf16 weights per layer, {L} distinct layers per "
+               "step); no flush"),
         "e2e": {"value": e2e_ms / L, "unit": "ms/layer", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                 "api": "paper_2602_00397_b200.sparse_ffn_layer (x from pinned host f32)",
@@ -625,6 +678,7 @@ def run_gpu(args, rank: int, world: int) -> None:
                                   "far below the HBM roof by design"),
         "kernels_timing": "CUDA events around each launch, in a second (instrumented) run of the same steps",
         "clocks": clocks,
+        "predictor_f32_input": f32_variant,
     }
 
     # ---- dense baselines on one layer (rank 0 only, single GPU)
@@ -660,12 +714,20 @@ def run_gpu(args, rank: int, world: int) -> None:
     del layers
     torch.cuda.empty_cache()
 
-    # ---- CPU baseline (rank 0, N=1): the oracle port on a bounded sample
+    # ---- CPU baseline (rank 0, N=1): the reference's own implementation (baseline/_ref,
+    # unmodified) on the host cores, else the oracle port, on a bounded sample
     if rank == 0 and world == 1 and not args.skip_cpu:
-        ms, info = cpu_sample(args.config, "port")
+        kind = "reference"
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+            import sparseprefill  # noqa: F401
+        except ImportError:
+            kind = "port"
+        ms, info = cpu_sample(args.config, kind)
         out["cpu_baseline"] = {
-            "value": ms, "unit": "ms/layer", "cores": cores(), "kind": "port",
-            "sample": f"oracle port, 1 dense + 1 predicted 128-token block of one layer "
+            "value": ms, "unit": "ms/layer", "cores": cores(), "kind": kind,
+            "sample": f"{'unmodified reference package' if kind == 'reference' else 'oracle port'}"
+                      f", 1 dense + 1 predicted 128-token block of one layer "
                       f"(t_dense {info['t_dense_block_s']:.2f}s, t_pred "
                       f"{info['t_sparse_block_s']:.2f}s), extrapolated to "
                       f"{info['n_blocks']} blocks"}
@@ -685,6 +747,8 @@ def main():
     ap.add_argument("--skip-dense", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-ttft", action="store_true")
+    ap.add_argument("--skip-f32-pred", action="store_true",
+                    help="skip timing the f32-predictor-input variant")
     ap.add_argument("--collective", default="nccl", choices=["nccl", "fused", "overlap"],
                     help="TP completion: NCCL all-reduce, the fused peer-memory kernel, or "
                          "that kernel overlapped with the down projection block by block")

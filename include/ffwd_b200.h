@@ -79,6 +79,15 @@ FFWD_API int ffwd_predictor_forward(const void* x, int x_is_f32, int T, int d, i
                            size_t workspace_bytes, void* stream);
 
 /*
+ * The predictor's first pooling pass alone (predictor.py:76): logits[t] =
+ * f32(q . x_t) / f32(sqrt d) for every row t of x [T x d] (bf16, or f32 when
+ * x_is_f32), f64 accumulation in the fixed order the fused RMSNorm producer shares
+ * (ffwd_rmsnorm_ex), so either source gives bit-identical logits.  d % 4 == 0.
+ */
+FFWD_API int ffwd_predictor_logits(const void* x, int x_is_f32, int T, int d, const float* query,
+                                   float* logits, void* stream);
+
+/*
  * Per-row top-k.  Replaces kernels.py:139-149 topk_indices / sparse.py:49-55 build_mask:
  * ties keep the lower index, -0 == +0, NaN after every number, result ascending.
  * idx_global [n_rows x ld_global] (nullable) receives global neuron ids; with
@@ -207,6 +216,20 @@ FFWD_API int ffwd_rmsnorm(float* x, const float* gain, int T, int d, double eps,
                           const void* add, int add_kind, void* out_bf16, float* out_f32,
                           const float* query, float* logits, int logit_row0, int logit_row1,
                           void* stream);
+
+/*
+ * ffwd_rmsnorm with flags.  FFWD_NORM_LOGITS_F32: the logits are f32(q . out_f32_t) /
+ * f32(sqrt d), i.e. dotted with the f32 output instead of its bf16 rounding (needs
+ * out_f32); the predictor then pools that f32 copy (ffwd_ffn_layer2's x_pred_f32), as
+ * the reference's predictor sees the f32 FFN input (engine.py:267, :286).  Either way
+ * the f64 summation order is the one ffwd_predictor_forward's own first pass uses, so
+ * the fused logits are bit-identical to the unfused ones.
+ */
+#define FFWD_NORM_LOGITS_F32 1
+FFWD_API int ffwd_rmsnorm_ex(float* x, const float* gain, int T, int d, double eps,
+                             const void* add, int add_kind, void* out_bf16, float* out_f32,
+                             const float* query, float* logits, int logit_row0, int logit_row1,
+                             int flags, void* stream);
 
 /*
  * apply_rope (engine.py:50-68) in place on Q and K of one [T x row_stride]

@@ -30,6 +30,7 @@ SIGNATURES = {
     "ffwd_predictor_workspace_bytes": (_c_size, [_c_int, _c_int, _c_int, _c_int]),
     "ffwd_predictor_forward": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp,
                                         _vp, _c_int, _c_int, _vp, _vp, _c_size, _vp]),
+    "ffwd_predictor_logits": (_c_int, [_vp, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
     "ffwd_topk": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp,
                            _c_int, _vp, _vp]),
     "ffwd_predict_topk": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp,
@@ -56,6 +57,8 @@ SIGNATURES = {
                                      _c_size, _vp]),
     "ffwd_rmsnorm": (_c_int, [_vp, _vp, _c_int, _c_int, ctypes.c_double, _vp, _c_int, _vp, _vp,
                               _vp, _vp, _c_int, _c_int, _vp]),
+    "ffwd_rmsnorm_ex": (_c_int, [_vp, _vp, _c_int, _c_int, ctypes.c_double, _vp, _c_int, _vp,
+                                 _vp, _vp, _vp, _c_int, _c_int, _c_int, _vp]),
     "ffwd_rope": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp,
                            _vp, _c_int, _vp]),
     "ffwd_ckpt_last_error": (ctypes.c_char_p, []),

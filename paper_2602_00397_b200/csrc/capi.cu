@@ -354,6 +354,20 @@ int ffwd_predictor_forward(const void* x, int x_is_f32, int T, int d, int blk_be
                        scores, static_cast<cudaStream_t>(stream));
 }
 
+int ffwd_predictor_logits(const void* x, int x_is_f32, int T, int d, const float* query,
+                          float* logits, void* stream) {
+  g_err.clear();
+  if (!x || !query || !logits) return fail(FFWD_ERR_VALIDATION, "predictor_logits: null pointer");
+  if (T < 1 || d < 4 || d % 4 != 0)
+    return fail(FFWD_ERR_VALIDATION, "predictor_logits dims T=%d d=%d (d %% 4 == 0)", T, d);
+  if (d > 16384) return fail(FFWD_ERR_UNSUPPORTED, "predictor_logits: d_model <= 16384");
+  const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));  // predictor.py:76
+  FFWD_CUDA(launch_logits_only(x, x_is_f32 != 0, d, 0, T, query, sqrt_d, logits,
+                               static_cast<cudaStream_t>(stream)),
+            "predictor_logits");
+  return FFWD_OK;
+}
+
 int ffwd_topk(const float* scores, int n_rows, int f, int k, int tp_rank, int tp_size,
               int32_t* idx_global, int ld_global, int32_t* idx_local, int ld_local,
               int32_t* counts, void* stream) {
@@ -774,7 +788,18 @@ int ffwd_ffn_layer_tp_overlap(const void* x_bf16, int T, int d, const void* wgu_
 int ffwd_rmsnorm(float* x, const float* gain, int T, int d, double eps, const void* add,
                  int add_kind, void* out_bf16, float* out_f32, const float* query, float* logits,
                  int logit_row0, int logit_row1, void* stream) {
+  return ffwd_rmsnorm_ex(x, gain, T, d, eps, add, add_kind, out_bf16, out_f32, query, logits,
+                         logit_row0, logit_row1, 0, stream);
+}
+
+int ffwd_rmsnorm_ex(float* x, const float* gain, int T, int d, double eps, const void* add,
+                    int add_kind, void* out_bf16, float* out_f32, const float* query,
+                    float* logits, int logit_row0, int logit_row1, int flags, void* stream) {
   g_err.clear();
+  if (!x || !gain) return fail(FFWD_ERR_VALIDATION, "rmsnorm needs x and gain");
+  if (flags & ~FFWD_NORM_LOGITS_F32) return fail(FFWD_ERR_VALIDATION, "unknown rmsnorm flags %d", flags);
+  if ((flags & FFWD_NORM_LOGITS_F32) && query && !out_f32)
+    return fail(FFWD_ERR_VALIDATION, "f32 logits need the f32 output the predictor pools");
   if (T < 1 || d < 4 || d % 4 != 0)
     return fail(FFWD_ERR_VALIDATION, "rmsnorm dims T=%d d=%d (d must be a positive multiple of 4)",
                 T, d);
@@ -789,7 +814,7 @@ int ffwd_rmsnorm(float* x, const float* gain, int T, int d, double eps, const vo
   StageTimer tm(kNorm, static_cast<cudaStream_t>(stream));
   FFWD_CUDA(launch_rmsnorm(x, gain, T, d, eps, add, add ? add_kind : 0, out_bf16, out_f32, query,
                            sqrt_d, logits, logit_row0, logit_row1,
-                           static_cast<cudaStream_t>(stream)),
+                           (flags & FFWD_NORM_LOGITS_F32) != 0, static_cast<cudaStream_t>(stream)),
             "rmsnorm");
   return FFWD_OK;
 }

@@ -46,11 +46,14 @@ struct PlanCounts {
 cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begin,
                         int blk_count, const float* query, float sqrt_d, float* logits,
                         float* pooled, const float* logits_in, cudaStream_t s);
+// First pass alone: logits[t] for rows [tok0, tok0 + ntok) of x.
+cudaError_t launch_logits_only(const void* x, bool x_is_f32, int d, int tok0, int ntok,
+                               const float* query, float sqrt_d, float* logits, cudaStream_t s);
 // FFN-input producers of the full prefill (norm.cu).
 cudaError_t launch_rmsnorm(float* x, const float* gain, int T, int d, double eps,
                            const void* add, int add_kind, void* out_bf16, float* out_f32,
                            const float* query, float sqrt_d, float* logits, int logit_row0,
-                           int logit_row1, cudaStream_t s);
+                           int logit_row1, bool logits_from_f32, cudaStream_t s);
 // Fused tensor-parallel completion (allreduce.cu): out_p = residual + sum_q partial_q on
 // every rank p (peer pointers), optional bf16 copy; flags: per-rank [2n + 1] words.
 cudaError_t launch_allreduce_residual(const float* const* partial, float* const* out,

@@ -24,38 +24,23 @@
 
 #include "ffwd_internal.h"
 #include "launch.cuh"
+#include "rowdot.cuh"
 
 namespace ffwd {
 
 namespace {
 
-constexpr int kNormThreads = 256;
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Sum over the CTA in warp order (fixed, deterministic).
-__device__ __forceinline__ double block_sum(double v, double* red) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  v = warp_sum(v);
-  __syncthreads();  // `red` may still be read from a previous call
-  if (lane == 0) red[warp] = v;
-  __syncthreads();
-  double s = 0.0;
-#pragma unroll
-  for (int w = 0; w < kNormThreads / 32; ++w) s += red[w];
-  return s;
-}
+constexpr int kNormThreads = rowdot::kThreads;  // the logit's summation layout (rowdot.cuh)
+using rowdot::block_sum;
 
 // Persistent CTAs (2 per SM) walk rows r = blockIdx.x + k gridDim.x; thread i owns the
 // float4 groups {i + 256 j} of a row.  The f32 -> f64 widening (F2F, 16 per clock per
 // SM) bounds this kernel, so the gain and the predictor query are widened once per CTA
 // into registers, each x element once (reused for the square and the output), and the
 // next row's loads are issued before the current row's reductions.
-template <int kMaxV, int kAdd>
+// kLogitF32: the logits are dotted with the f32 outputs (the predictor then pools the
+// f32 copy, the reference's own f32 FFN input) instead of their bf16 roundings.
+template <int kMaxV, int kAdd, bool kLogitF32>
 __global__ void __launch_bounds__(kNormThreads, 2)
     rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ gain, int T, int d,
                    double eps, const void* __restrict__ add, __nv_bfloat16* __restrict__ out_bf16,
@@ -147,16 +132,18 @@ __global__ void __launch_bounds__(kNormThreads, 2)
         pk.y = *reinterpret_cast<const uint32_t*>(&hi);
         reinterpret_cast<uint2*>(out_bf16 + off)[0] = pk;
       }
-      if (want_logit) {  // q . bf16(x), the operand the pooling pass would read
-        const float2 l2 = __bfloat1622float2(lo), h2 = __bfloat1622float2(hi);
-        z[0] = fma(qd[j][0], static_cast<double>(l2.x), z[0]);
-        z[1] = fma(qd[j][1], static_cast<double>(l2.y), z[1]);
-        z[2] = fma(qd[j][2], static_cast<double>(h2.x), z[2]);
-        z[3] = fma(qd[j][3], static_cast<double>(h2.y), z[3]);
+      if (want_logit) {  // q . x with x the operand the pooling pass reads
+        if constexpr (kLogitF32) {
+          rowdot::accumulate(z, qd[j], o);
+        } else {
+          const float2 l2 = __bfloat1622float2(lo), h2 = __bfloat1622float2(hi);
+          const float xb[4] = {l2.x, l2.y, h2.x, h2.y};
+          rowdot::accumulate(z, qd[j], xb);
+        }
       }
     }
     if (want_logit) {
-      const double zs = block_sum((z[0] + z[1]) + (z[2] + z[3]), red);
+      const double zs = block_sum(rowdot::thread_value(z), red);
       if (threadIdx.x == 0)
         logits[row - logit_row0] = __fdiv_rn(static_cast<float>(zs), sqrt_d);  // predictor.py:76
     }
@@ -225,7 +212,7 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace
 
-template <int kAdd>
+template <int kAdd, bool kLogitF32>
 cudaError_t launch_rmsnorm_t(float* x, const float* gain, int T, int d, double eps,
                              const void* add, __nv_bfloat16* ob, float* out_f32,
                              const float* query, float sqrt_d, float* logits, int r0, int r1,
@@ -237,7 +224,7 @@ cudaError_t launch_rmsnorm_t(float* x, const float* gain, int T, int d, double e
   const int grid = T < 2 * sms ? T : 2 * sms;
   cudaError_t e = cudaSuccess;
 #define FFWD_NORM(V)                                                                       \
-  e = launch_k(rmsnorm_kernel<V, kAdd>, dim3(grid), dim3(kNormThreads), 0, s, 1, x, gain, T, d, \
+  e = launch_k(rmsnorm_kernel<V, kAdd, kLogitF32>, dim3(grid), dim3(kNormThreads), 0, s, 1, x, gain, T, d, \
                eps, add, ob, out_f32, query, sqrt_d, logits, r0, r1)
   if (nv <= 1) FFWD_NORM(1);
   else if (nv <= 2) FFWD_NORM(2);
@@ -249,20 +236,32 @@ cudaError_t launch_rmsnorm_t(float* x, const float* gain, int T, int d, double e
   return e;
 }
 
+template <bool kLogitF32>
+cudaError_t launch_rmsnorm_l(float* x, const float* gain, int T, int d, double eps,
+                             const void* add, int add_kind, __nv_bfloat16* ob, float* out_f32,
+                             const float* query, float sqrt_d, float* logits, int logit_row0,
+                             int logit_row1, cudaStream_t s) {
+  if (add == nullptr || add_kind == 0)
+    return launch_rmsnorm_t<0, kLogitF32>(x, gain, T, d, eps, nullptr, ob, out_f32, query, sqrt_d,
+                                          logits, logit_row0, logit_row1, s);
+  if (add_kind == 1)
+    return launch_rmsnorm_t<1, kLogitF32>(x, gain, T, d, eps, add, ob, out_f32, query, sqrt_d,
+                                          logits, logit_row0, logit_row1, s);
+  return launch_rmsnorm_t<2, kLogitF32>(x, gain, T, d, eps, add, ob, out_f32, query, sqrt_d,
+                                        logits, logit_row0, logit_row1, s);
+}
+
 cudaError_t launch_rmsnorm(float* x, const float* gain, int T, int d, double eps,
                            const void* add, int add_kind, void* out_bf16, float* out_f32,
                            const float* query, float sqrt_d, float* logits, int logit_row0,
-                           int logit_row1, cudaStream_t s) {
+                           int logit_row1, bool logits_from_f32, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   auto* ob = static_cast<__nv_bfloat16*>(out_bf16);
-  if (add == nullptr || add_kind == 0)
-    return launch_rmsnorm_t<0>(x, gain, T, d, eps, nullptr, ob, out_f32, query, sqrt_d, logits,
-                               logit_row0, logit_row1, s);
-  if (add_kind == 1)
-    return launch_rmsnorm_t<1>(x, gain, T, d, eps, add, ob, out_f32, query, sqrt_d, logits,
-                               logit_row0, logit_row1, s);
-  return launch_rmsnorm_t<2>(x, gain, T, d, eps, add, ob, out_f32, query, sqrt_d, logits,
-                             logit_row0, logit_row1, s);
+  if (logits_from_f32 && query != nullptr)
+    return launch_rmsnorm_l<true>(x, gain, T, d, eps, add, add_kind, ob, out_f32, query, sqrt_d,
+                                  logits, logit_row0, logit_row1, s);
+  return launch_rmsnorm_l<false>(x, gain, T, d, eps, add, add_kind, ob, out_f32, query, sqrt_d,
+                                 logits, logit_row0, logit_row1, s);
 }
 
 cudaError_t launch_rope(void* qk, bool is_f32, int T, int row_stride, int k_col, int n_heads,

@@ -1,8 +1,9 @@
 // K1a/K1b: the FastForward expert predictor (predictor.py:68-81), fp64-exact.
 //
-//   logits_kernel   one warp per token: logit_t = f32(q . x_t) / f32(sqrt d), the dot
-//                   product accumulated in f64 and rounded once (kernels.py:41-54), the
-//                   divide a true IEEE f32 division (predictor.py:76).
+//   logits_kernel   one CTA per token row: logit_t = f32(q . x_t) / f32(sqrt d), the dot
+//                   product accumulated in f64 in the fixed order of rowdot.cuh (shared
+//                   with the fused RMSNorm producer) and rounded once (kernels.py:41-54),
+//                   the divide a true IEEE f32 division (predictor.py:76).
 //   pooled_kernel   per (block, 256 columns): p = f32(softmax_f64(logits_b))
 //                   (kernels.py:57-80), pooled = f32(sum_t p_t x_t) in f64 (:78).
 //                   Runs the blocks in reverse so the rows pass 1 read last hit L2.
@@ -32,6 +33,7 @@
 #ifndef FFWD_POOL_MINB
 #define FFWD_POOL_MINB 3
 #endif
+#include "rowdot.cuh"
 #include "sm100.cuh"
 
 namespace ffwd {
@@ -80,58 +82,94 @@ struct Raw8 {
   }
 };
 
-constexpr int kLogitThreads = 256;
-constexpr int kLogitWarps = kLogitThreads / 32;
+constexpr int kLogitThreads = rowdot::kThreads;
 constexpr int kPoolThreads = 256;
 constexpr int kPoolCols = 512;   // per CTA: two 256-column warp halves
 constexpr int kPoolQuarters = 4; // token quarters of a block
 
+// 4 consecutive activations (bf16 or f32) of a row, widened to f32 (exact).
+template <bool kF32>
+__device__ __forceinline__ void load4(const void* base, size_t elem, float (&v)[4]) {
+  if constexpr (kF32) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(static_cast<const float*>(base) + elem));
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else {
+    const uint2 t = __ldg(reinterpret_cast<const uint2*>(
+        static_cast<const __nv_bfloat16*>(base) + elem));
+    v[0] = __uint_as_float(t.x << 16); v[1] = __uint_as_float(t.x & 0xFFFF0000u);
+    v[2] = __uint_as_float(t.y << 16); v[3] = __uint_as_float(t.y & 0xFFFF0000u);
+  }
+}
+
 // Pass 1: logit_t = f32(q . x_t) / f32(sqrt d) for every token of the predicted blocks
 // (predictor.py:76; the matmul accumulates in f64 and rounds once, kernels.py:41-54).
-// One warp per token row, 4 x 16 B loads per lane in flight, 40 registers so 64 warps
-// per SM stay resident.  (A/B on B200, ncu, 8B/16K: this 39 us; q held in f64
-// registers with one widening per x element 49 us; q in f64 shared memory 78 us.)
-template <bool kF32>
+// One 256-thread CTA per row at a time, in the summation order of rowdot.cuh -- the same
+// order the fused RMSNorm producer uses, so a logit is bit-identical whichever kernel
+// computes it.  Persistent CTAs walk rows with the next row's loads in flight during the
+// current row's reduction.  q is widened into registers once per CTA.
+template <bool kF32, int kMaxV>
 __global__ void __launch_bounds__(kLogitThreads)
     logits_kernel(const void* __restrict__ x, int d, int tok0, int ntok,
                   const float* __restrict__ query, float sqrt_d, float* __restrict__ logits) {
+  __shared__ double red[rowdot::kWarps];
+  const int nv = d / 4;
+  double qd[kMaxV][4];
+#pragma unroll
+  for (int j = 0; j < kMaxV; ++j) {
+    const int g = threadIdx.x + kLogitThreads * j;
+    const float4 q = g < nv ? __ldg(reinterpret_cast<const float4*>(query) + g)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    qd[j][0] = q.x; qd[j][1] = q.y; qd[j][2] = q.z; qd[j][3] = q.w;
+  }
   pdl_wait();
   pdl_trigger();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t = blockIdx.x * kLogitWarps + warp;
-  if (t >= ntok) return;
-  const size_t row = static_cast<size_t>(tok0 + t) * d;
-  const int ng = d / 8;
-  double a0 = 0.0, a1 = 0.0;
-  int g = lane;
-  for (; g + 96 < ng; g += 128) {  // 4 groups of 8 columns per lane per iteration
-    Raw8<kF32> xr[4];
-    Raw8<true> qr[4];
+  float nxt[kMaxV][4];
+  auto load_row = [&](int t) {
+    const size_t row = static_cast<size_t>(tok0 + t) * d;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) xr[u].load(x, row + 8 * static_cast<size_t>(g + 32 * u));
-#pragma unroll
-    for (int u = 0; u < 4; ++u) qr[u].load(query, 8 * static_cast<size_t>(g + 32 * u));
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        a0 = fma(qr[u].get(i), xr[u].get(i), a0);
-        a1 = fma(qr[u].get(4 + i), xr[u].get(4 + i), a1);
-      }
-  }
-  for (; g < ng; g += 32) {
-    Raw8<kF32> xr;
-    Raw8<true> qr;
-    xr.load(x, row + 8 * static_cast<size_t>(g));
-    qr.load(query, 8 * static_cast<size_t>(g));
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      a0 = fma(qr.get(i), xr.get(i), a0);
-      a1 = fma(qr.get(4 + i), xr.get(4 + i), a1);
+    for (int j = 0; j < kMaxV; ++j) {
+      const int g = threadIdx.x + kLogitThreads * j;
+      if (g < nv) load4<kF32>(x, row + 4 * static_cast<size_t>(g), nxt[j]);
     }
+  };
+  int t = blockIdx.x;
+  if (t < ntok) load_row(t);
+  for (; t < ntok; t += gridDim.x) {
+    float v[kMaxV][4];
+#pragma unroll
+    for (int j = 0; j < kMaxV; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[j][e] = nxt[j][e];
+    if (t + static_cast<int>(gridDim.x) < ntok) load_row(t + gridDim.x);
+    double z[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < kMaxV; ++j) {
+      const int g = threadIdx.x + kLogitThreads * j;
+      if (g < nv) rowdot::accumulate(z, qd[j], v[j]);
+    }
+    const double zs = rowdot::block_sum(rowdot::thread_value(z), red);
+    if (threadIdx.x == 0) logits[t] = __fdiv_rn(static_cast<float>(zs), sqrt_d);  // predictor.py:76
   }
-  const double z = warp_sum_f64(a0 + a1);
-  if (lane == 0) logits[t] = __fdiv_rn(static_cast<float>(z), sqrt_d);  // predictor.py:76
+}
+
+template <bool kF32>
+cudaError_t launch_logits(const void* x, int d, int tok0, int ntok, const float* query,
+                          float sqrt_d, float* logits, cudaStream_t s) {
+  const int nv = (d / 4 + kLogitThreads - 1) / kLogitThreads;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const dim3 grid(std::min(ntok, 8 * sms));
+#define FFWD_LOGITS(V)                                                                     \
+  return launch_k(logits_kernel<kF32, V>, grid, dim3(kLogitThreads), 0, s, 1, x, d, tok0, ntok, \
+                  query, sqrt_d, logits)
+  if (nv <= 1) FFWD_LOGITS(1);
+  if (nv <= 2) FFWD_LOGITS(2);
+  if (nv <= 4) FFWD_LOGITS(4);
+  if (nv <= 8) FFWD_LOGITS(8);
+  if (nv <= 16) FFWD_LOGITS(16);
+#undef FFWD_LOGITS
+  return cudaErrorInvalidValue;
 }
 
 // Pass 2: p = f32(softmax_f64(logits_b)) (kernels.py:57-80), recomputed by every CTA of
@@ -473,29 +511,33 @@ cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begi
   if (blk_count <= 0) return cudaSuccess;
   const int tok0 = blk_begin * kBlockTokens;
   const int ntok = std::min(T, (blk_begin + blk_count) * kBlockTokens) - tok0;
-  const dim3 g1((ntok + kLogitWarps - 1) / kLogitWarps);
   const dim3 g2((d + kPoolCols - 1) / kPoolCols, blk_count);
   // logits_in: precomputed by the producer of X (absolute token index), e.g. the fused
   // RMSNorm; the first pass is then skipped.
   const float* lg = logits_in ? logits_in + tok0 : logits;
   if (x_is_f32) {
     if (!logits_in) {
-      cudaError_t e = launch_k(logits_kernel<true>, g1, dim3(kLogitThreads), 0, s, 1, x, d, tok0,
-                               ntok, query, sqrt_d, logits);
+      cudaError_t e = launch_logits<true>(x, d, tok0, ntok, query, sqrt_d, logits, s);
       if (e != cudaSuccess) return e;
     }
     return launch_k(pooled_kernel<true>, g2, dim3(kPoolThreads), 0, s, 1, x, T, d, blk_begin,
                     blk_count, lg, pooled);
   } else {
     if (!logits_in) {
-      cudaError_t e = launch_k(logits_kernel<false>, g1, dim3(kLogitThreads), 0, s, 1, x, d, tok0,
-                               ntok, query, sqrt_d, logits);
+      cudaError_t e = launch_logits<false>(x, d, tok0, ntok, query, sqrt_d, logits, s);
       if (e != cudaSuccess) return e;
     }
     return launch_k(pooled_kernel<false>, g2, dim3(kPoolThreads), 0, s, 1, x, T, d, blk_begin,
                     blk_count, lg, pooled);
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_logits_only(const void* x, bool x_is_f32, int d, int tok0, int ntok,
+                               const float* query, float sqrt_d, float* logits, cudaStream_t s) {
+  if (ntok <= 0) return cudaSuccess;
+  return x_is_f32 ? launch_logits<true>(x, d, tok0, ntok, query, sqrt_d, logits, s)
+                  : launch_logits<false>(x, d, tok0, ntok, query, sqrt_d, logits, s);
 }
 
 template <int RG>

@@ -21,15 +21,23 @@ ROPE_BASE = 10000.0  # engine.py:41
 def rmsnorm(x: torch.Tensor, gain: torch.Tensor, eps: float = 1e-6, out_bf16: bool = True,
             out_f32: bool = False, predictor: DevicePredictor | None = None,
             logits: torch.Tensor | None = None, out: torch.Tensor | None = None,
-            out32: torch.Tensor | None = None, add: torch.Tensor | None = None):
+            out32: torch.Tensor | None = None, add: torch.Tensor | None = None,
+            logits_from_f32: bool = False):
     """Rows of x (T, d) f32 scaled to unit RMS times `gain` (f64 arithmetic, f32 result).
 
     With `add` ((T, d) f32 or bf16) the residual add ``x += add`` runs first, in place.
 
     Returns (bf16 or None, f32 or None, logits or None).  With `predictor`, also
     writes f32(q . bf16(row)) / f32(sqrt d) per row into `logits` (T,), the input of
-    the predictor's pooling pass (``sparse_ffn_layer(..., logits_in=...)``).
+    the predictor's pooling pass (``sparse_ffn_layer(..., logits_in=...)``); with
+    ``logits_from_f32`` the dot product takes the f32 row instead (needs ``out_f32``;
+    the predictor then pools that f32 copy: ``sparse_ffn_layer(..., x_pred_f32=...)``,
+    the reference's predictor input, ``engine.py:267,286``).  The f64 summation order
+    is the predictor's own (``csrc/rowdot.cuh``), so fused logits equal unfused ones bit
+    for bit.
     """
+    if logits_from_f32 and predictor is not None and not out_f32:
+        raise ValidationError("logits_from_f32 needs out_f32 (the predictor pools the f32 rows)")
     if not (x.is_cuda and x.dtype == torch.float32 and x.dim() == 2 and x.is_contiguous()):
         raise ValidationError("rmsnorm expects a contiguous CUDA f32 (T, d) tensor")
     T, d = x.shape
@@ -56,12 +64,12 @@ def rmsnorm(x: torch.Tensor, gain: torch.Tensor, eps: float = 1e-6, out_bf16: bo
             raise ValidationError("rmsnorm add must be a contiguous CUDA f32/bf16 (T, d) tensor")
         add_kind = 1 if add.dtype == torch.float32 else 2
     lib = _dev.lib_for(dev)
-    _lib.check(lib.ffwd_rmsnorm(x.data_ptr(), g.data_ptr(), T, d, float(eps), _dev.ptr(add),
-                                add_kind, _dev.ptr(ob),
-                                _dev.ptr(o32), _dev.ptr(q), _dev.ptr(logits if q is not None
-                                                                      else None),
-                                0, T if q is not None else 0, _dev.stream_handle(dev)),
-               "rmsnorm")
+    _lib.check(lib.ffwd_rmsnorm_ex(x.data_ptr(), g.data_ptr(), T, d, float(eps), _dev.ptr(add),
+                                   add_kind, _dev.ptr(ob), _dev.ptr(o32), _dev.ptr(q),
+                                   _dev.ptr(logits if q is not None else None), 0,
+                                   T if q is not None else 0,
+                                   1 if (logits_from_f32 and q is not None) else 0,
+                                   _dev.stream_handle(dev)), "rmsnorm")
     return ob, o32, (logits if q is not None else None)
 
 

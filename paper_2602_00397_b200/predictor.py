@@ -116,6 +116,23 @@ def predictor_scores(dp: DevicePredictor, x: torch.Tensor, blk_begin: int = 0,
     return scores
 
 
+def predictor_logits(dp: DevicePredictor, x: torch.Tensor) -> torch.Tensor:
+    """Per-token logits f32(q . x_t) / f32(sqrt d) (``predictor.py:76``) of a device
+    tensor x (T, d), f32 or bf16: the predictor's first pooling pass alone, in the f64
+    order the fused RMSNorm producer shares (``ffwd_predictor_logits``)."""
+    if x.dim() != 2 or x.shape[1] != dp.d:
+        raise ValidationError(f"predictor input shape {tuple(x.shape)}, d_model={dp.d}")
+    if x.dtype not in (torch.float32, torch.bfloat16):
+        x = x.float()
+    x = x.contiguous()
+    out = torch.empty((x.shape[0],), dtype=torch.float32, device=x.device)
+    lib = _dev.lib_for(x.device)
+    _lib.check(lib.ffwd_predictor_logits(x.data_ptr(), int(x.dtype == torch.float32), x.shape[0],
+                                         dp.d, dp.query.data_ptr(), out.data_ptr(),
+                                         _dev.stream_handle(x.device)), "predictor_logits")
+    return out
+
+
 def predictor_forward(params, x):
     """Neuron scores (d_ffn,) for one block of FFN inputs x (n, d_model).
 

@@ -3,8 +3,10 @@ restatements of the reference, and the whole prefill against the reference's own
 golden run (tests/golden/prefill_small.npz, made by engine.prefill_blockwise).
 
 Bars:
-  * rmsnorm (f64 arithmetic, f32 result) and the fused predictor logits: bit-exact
-    except for <= 1e-4 of elements 1 ulp apart (f64 summation order);
+  * rmsnorm (f64 arithmetic, f32 result): bit-exact except for <= 1e-4 of elements
+    1 ulp apart (f64 summation order vs NumPy);
+  * fused predictor logits: bit-identical to the predictor's own first pass (shared f64
+    order), and near-exact (same bar) against NumPy;
   * RoPE, f32 storage: bit-exact;
   * prefill, f32 attention (parity mode): layer-0 masks bit-exact, every mask >= 98%
     equal (later layers see bf16-FFN residuals), per-block hidden rel-L2 <= 1e-2 where
@@ -64,9 +66,21 @@ def test_rmsnorm_and_fused_logits(ff, T, d):
     want = rms_ref(x, gain)
     near_exact(x32.cpu().numpy(), want, "rmsnorm f32")
     assert np.array_equal(xb.float().cpu().numpy(), orc.bf16_round(x32.cpu().numpy()))
-    xr = orc.bf16_round(want)
+    # fused logits == the predictor's own first pass on the same bf16 rows, bit for bit
+    # (one f64 summation order, csrc/rowdot.cuh)
+    from paper_2602_00397_b200.predictor import predictor_logits
+    assert torch.equal(lg, predictor_logits(dp, xb)), "fused logits differ from the unfused pass"
+    # ... and near the NumPy restatement (its dgemm order is OpenBLAS's, not pinned)
+    xr = orc.bf16_round(x32.cpu().numpy())
     z = orc.mm(pred["query"], xr.T)[0] / np.float32(np.sqrt(d))  # predictor.py:76
     near_exact(lg.cpu().numpy(), z.astype(np.float32), "fused logits")
+    # f32 mode: logits dotted with the f32 rows (the reference's predictor input)
+    _, x32b, lg32 = rmsnorm(torch.from_numpy(x).cuda(), torch.from_numpy(gain).cuda(),
+                            out_f32=True, predictor=dp, logits_from_f32=True)
+    assert torch.equal(x32b, x32)
+    assert torch.equal(lg32, predictor_logits(dp, x32)), "f32 fused logits differ"
+    z32 = orc.mm(pred["query"], x32.cpu().numpy().T)[0] / np.float32(np.sqrt(d))
+    near_exact(lg32.cpu().numpy(), z32.astype(np.float32), "fused f32 logits")
 
 
 @pytest.mark.parametrize("add_dtype", [torch.float32, torch.bfloat16])
