@@ -79,6 +79,18 @@ FFWD_API int ffwd_predictor_forward(const void* x, int x_is_f32, int T, int d, i
                            size_t workspace_bytes, void* stream);
 
 /*
+ * predictor_forward (predictor.py:68-81) for ONE block of any n rows and any d_model:
+ * the reference pools whatever block it is handed (n = 1 .. 25600 here), so the drop-in
+ * accepts what it accepts.  x [n x d] (bf16, or f32 when x_is_f32); scores [f] f32;
+ * workspace >= ffwd_predictor_workspace_bytes(1, d, r, f).  Same f64 accumulation and
+ * f32 rounding points as ffwd_predictor_forward.
+ */
+FFWD_API int ffwd_predictor_forward_block(const void* x, int x_is_f32, int n, int d,
+                                          const float* query, const float* w1, const float* w2,
+                                          int r, int f, float* scores, void* workspace,
+                                          size_t workspace_bytes, void* stream);
+
+/*
  * The predictor's first pooling pass alone (predictor.py:76): logits[t] =
  * f32(q . x_t) / f32(sqrt d) for every row t of x [T x d] (bf16, or f32 when
  * x_is_f32), f64 accumulation in the fixed order the fused RMSNorm producer shares

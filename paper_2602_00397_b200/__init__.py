@@ -9,7 +9,7 @@ kernels (``libffwd_b200.so``) behind a C-ABI (``include/ffwd_b200.h``).
 from .errors import NumericError, UnsupportedError, ValidationError
 from .model import LayerWeights, ModelConfig
 from .predictor import (DevicePredictor, PredictorParams, default_reduced_dim, init_predictor,
-                        predictor_forward, predictor_scores)
+                        predictor_forward, predictor_logits, predictor_scores)
 from .compensator import (CompensatorParams, apply_compensation, compensator_forward,
                           default_comp_dim, init_compensator)
 from .sparse import (ExpertMask, FirstBlockStatic, SubWeights, budget_to_k, build_mask,
@@ -18,7 +18,8 @@ from .sparse import (ExpertMask, FirstBlockStatic, SubWeights, budget_to_k, buil
 from .scheduler import (AttentionMassProfile, SparsityPlan, allocate_budgets, budgets_to_topk,
                         dense_plan, load_plan, plan_from_profile, save_plan, uniform_plan)
 from .costmodel import FlopsReport, ffn_path_flops, predict_prefill_flops
-from .layer import (PackedLayer, dense_ffn, ffn_layer_mode, oracle_scores, pack_layer,
+from .layer import (PackedLayer, dense_ffn, ffn_layer_mode, invalidate_packed, oracle_scores,
+                    pack_layer,
                     run_sparse_ffn, seq_shard, set_raster, shard_comp_cols, shard_neurons,
                     sparse_ffn_layer)
 

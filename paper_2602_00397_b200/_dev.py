@@ -6,6 +6,8 @@ hot path happens in libffwd_b200.so.
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 import torch
 
@@ -43,17 +45,62 @@ def lib_for(device: torch.device):
     return _lib.require_device(device.index if device.index is not None else 0)
 
 
-_ws: dict[int, torch.Tensor] = {}
+_ws: dict[tuple[int, int], torch.Tensor] = {}
+_ws_lock = threading.Lock()
 
 
 def workspace(device: torch.device, nbytes: int) -> torch.Tensor:
-    """A per-device scratch buffer that only grows (stream-ordered reuse)."""
+    """Scratch for the current stream of `device`, grow-only, one buffer per stream.
+
+    Calls on the same stream are ordered, so they can share one buffer; two streams
+    never do.  A grown buffer replaces the old one, whose memory the caching allocator
+    hands back only to work on the same stream (its allocation stream), after the work
+    already queued there, so in-flight kernels never see it reused."""
     idx = device.index if device.index is not None else 0
-    buf = _ws.get(idx)
-    if buf is None or buf.numel() < nbytes:
-        buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
-        _ws[idx] = buf
-    return buf
+    key = (idx, torch.cuda.current_stream(device).cuda_stream)
+    with _ws_lock:
+        buf = _ws.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+            _ws[key] = buf
+        return buf
+
+
+def fingerprint(*arrays) -> tuple:
+    """Cheap identity + content key of host / device arrays, for caches of derived device
+    data (packed weights): the buffer address, shape and dtype, plus torch's in-place
+    version counter for tensors or a strided content sample for numpy arrays (an in-place
+    edit of a numpy array that misses every sampled element is not seen: call
+    ``layer.invalidate_packed`` after editing weights in place)."""
+    key = []
+    for a in arrays:
+        if a is None:
+            key.append(None)
+        elif isinstance(a, torch.Tensor):
+            key.append(("t", a.data_ptr(), tuple(a.shape), str(a.dtype), a._version))
+        else:
+            arr = np.asarray(a)
+            flat = arr.reshape(-1)
+            step = max(1, flat.size // 4096)
+            sample = np.ascontiguousarray(flat[::step])
+            key.append(("n", arr.__array_interface__["data"][0], arr.shape, arr.dtype.str,
+                        hash(sample.tobytes())))
+    return tuple(key)
+
+
+def cached_on(obj, slot: str, key, build):
+    """`build()` memoised on `obj` itself (its ``__dict__``) under `slot`, valid while `key`
+    (a fingerprint) is unchanged.  The cache lives and dies with the object, so no global
+    table keyed by ``id()`` can go stale."""
+    store = getattr(obj, "__dict__", None)
+    if store is None:
+        return build()
+    hit = store.get(slot)
+    if hit is not None and hit[0] == key:
+        return hit[1]
+    val = build()
+    store[slot] = (key, val)
+    return val
 
 
 def is_host(a) -> bool:

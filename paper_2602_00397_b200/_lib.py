@@ -30,6 +30,8 @@ SIGNATURES = {
     "ffwd_predictor_workspace_bytes": (_c_size, [_c_int, _c_int, _c_int, _c_int]),
     "ffwd_predictor_forward": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp,
                                         _vp, _c_int, _c_int, _vp, _vp, _c_size, _vp]),
+    "ffwd_predictor_forward_block": (_c_int, [_vp, _c_int, _c_int, _c_int, _vp, _vp, _vp, _c_int,
+                                              _c_int, _vp, _vp, _c_size, _vp]),
     "ffwd_predictor_logits": (_c_int, [_vp, _c_int, _c_int, _c_int, _vp, _vp, _vp]),
     "ffwd_topk": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp,
                            _c_int, _vp, _vp]),

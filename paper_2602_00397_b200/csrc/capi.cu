@@ -8,6 +8,8 @@
 #include <cstring>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -22,17 +24,20 @@ using namespace ffwd;
 namespace {
 
 thread_local std::string g_err;
-int g_up_group = 32;
-int g_serpentine = 1;
+// Process-wide tuning knobs: atomics, so a knob set from one thread is read whole by
+// launches on any other (each launch reads each knob once; calls stay re-entrant).
+std::atomic<int> g_up_group{32};
+std::atomic<int> g_serpentine{1};
 #ifndef FFWD_BLOCKDEP_DEFAULT
 #define FFWD_BLOCKDEP_DEFAULT 1
 #endif
-int g_blockdep = FFWD_BLOCKDEP_DEFAULT;
+std::atomic<int> g_blockdep{FFWD_BLOCKDEP_DEFAULT};
 #ifndef FFWD_PDL_DEFAULT
 #define FFWD_PDL_DEFAULT 1
 #endif
-int g_pdl = FFWD_PDL_DEFAULT;
-int g_down_group = 16;  // ncu sweep: K3 DRAM 3.0 GB -> 1.7 GB per layer vs 8 (profiles/r1_raster_sweep.txt)
+std::atomic<int> g_pdl{FFWD_PDL_DEFAULT};
+// ncu sweep: K3 DRAM 3.0 GB -> 1.7 GB per layer vs 8 (profiles/r1_raster_sweep.txt)
+std::atomic<int> g_down_group{16};
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -60,16 +65,18 @@ int rup(int v, int m) { return (v + m - 1) / m * m; }
 enum Stage { kPool = 0, kW1, kW2, kTopk, kPlan, kUp, kDown, kNorm, kNumStages };
 const char* kStageNames[kNumStages] = {"pool", "predictor_w1", "predictor_w2", "topk",
                                        "plan", "up_proj", "down_proj", "ffn_norm"};
-bool g_timing = false;
+std::atomic<bool> g_timing{false};
 struct Rec {
   int stage;
   int kernels;  // kernel launches inside the timed stage
   cudaEvent_t a, b;
 };
+std::mutex g_rec_mu;  // guards g_recs and g_event_pool (launches may come from any thread)
 std::vector<Rec> g_recs;
 std::vector<cudaEvent_t> g_event_pool;
 
 cudaEvent_t take_event() {
+  std::lock_guard<std::mutex> lk(g_rec_mu);
   if (!g_event_pool.empty()) {
     cudaEvent_t e = g_event_pool.back();
     g_event_pool.pop_back();
@@ -94,6 +101,7 @@ struct StageTimer {
   ~StageTimer() {
     if (r.stage < 0) return;
     cudaEventRecord(r.b, s);
+    std::lock_guard<std::mutex> lk(g_rec_mu);
     g_recs.push_back(r);
   }
 };
@@ -145,7 +153,12 @@ int run_predictor(const void* x, bool x_is_f32, int T, int d, int b0, int nb, co
                   const float* w1, const float* w2, int r, int f, const Pred& p, float* scores,
                   cudaStream_t s, const float* logits_in = nullptr) {
   const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));  // predictor.py:76
-  {
+  if (d % 8 != 0) {  // any-shape pooling (small drop-in shapes; no fused logits)
+    StageTimer tm(kPool, s);
+    FFWD_CUDA(launch_pool_generic(x, x_is_f32, T, d, kBlockTokens, b0, nb, query, sqrt_d,
+                                  p.pooled, s),
+              "pool");
+  } else {
     StageTimer tm(kPool, s, logits_in ? 1 : 2);
     FFWD_CUDA(launch_pool(x, x_is_f32, T, d, b0, nb, query, sqrt_d, p.logits, p.pooled, logits_in, s),
               "pool");
@@ -228,14 +241,14 @@ int run_ffn(const void* x, int T, int d, const void* wgu_t, const void* wd, int 
   pa.counts = counts;
   pa.idx_shared = idx_shared;
   pa.has_comp = has_comp;
-  pa.up_group = g_up_group;
-  pa.down_group = g_down_group;
+  pa.up_group = g_up_group.load(std::memory_order_relaxed);
+  pa.down_group = g_down_group.load(std::memory_order_relaxed);
   pa.bn_down = bn_for(d);
   pa.hcols_alloc = w.hcols;
-  pa.serpentine = g_serpentine;
+  pa.serpentine = g_serpentine.load(std::memory_order_relaxed);
   pa.pair_up = up_proj_paired() ? 1 : 0;
   pa.pair_down = down_proj_paired() ? 1 : 0;
-  pa.blk_done = (g_blockdep && !up_only) ? w.blk_done : nullptr;
+  pa.blk_done = (g_blockdep.load(std::memory_order_relaxed) && !up_only) ? w.blk_done : nullptr;
   {
     StageTimer tm(kPlan, s);
     FFWD_CUDA(launch_plan(pa, w.meta, w.up, w.up_cap, w.down, w.down_cap, w.pc, s), "plan");
@@ -290,7 +303,7 @@ int check_gemm_shapes(int d, int f_local) {
 }  // namespace
 
 namespace ffwd {
-bool pdl_enabled() { return g_pdl != 0; }
+bool pdl_enabled() { return g_pdl.load(std::memory_order_relaxed) != 0; }
 }  // namespace ffwd
 
 extern "C" {
@@ -322,8 +335,8 @@ int ffwd_set_serpentine(int on) {
 int ffwd_set_raster(int up_group, int down_group) {
   if (up_group < 1 || down_group < 1)
     return fail(FFWD_ERR_VALIDATION, "raster groups must be >= 1");
-  g_up_group = up_group;
-  g_down_group = down_group;
+  g_up_group.store(up_group);
+  g_down_group.store(down_group);
   return FFWD_OK;
 }
 
@@ -340,8 +353,8 @@ int ffwd_predictor_forward(const void* x, int x_is_f32, int T, int d, int blk_be
   g_err.clear();
   if (T < 1 || d < 1 || r < 1 || f < 1)
     return fail(FFWD_ERR_VALIDATION, "predictor dims T=%d d=%d r=%d f=%d", T, d, r, f);
-  if (d % 8 != 0)
-    return fail(FFWD_ERR_UNSUPPORTED, "predictor needs d_model %% 8 == 0, got %d", d);
+  if (!x || !query || !w1 || !w2 || !scores || (blk_count > 0 && !workspace))
+    return fail(FFWD_ERR_VALIDATION, "predictor_forward: null pointer");
   const int n_blk = (T + kBlockTokens - 1) / kBlockTokens;
   if (blk_begin < 0 || blk_count < 0 || blk_begin + blk_count > n_blk)
     return fail(FFWD_ERR_VALIDATION, "block range [%d, %d) outside [0, %d)", blk_begin,
@@ -352,6 +365,29 @@ int ffwd_predictor_forward(const void* x, int x_is_f32, int T, int d, int blk_be
   Pred p = carve_pred(c, blk_count, d, r, f, false);
   return run_predictor(x, x_is_f32 != 0, T, d, blk_begin, blk_count, query, w1, w2, r, f, p,
                        scores, static_cast<cudaStream_t>(stream));
+}
+
+int ffwd_predictor_forward_block(const void* x, int x_is_f32, int n, int d, const float* query,
+                                 const float* w1, const float* w2, int r, int f, float* scores,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  if (n < 1 || d < 1 || r < 1 || f < 1)
+    return fail(FFWD_ERR_VALIDATION, "predictor dims n=%d d=%d r=%d f=%d", n, d, r, f);
+  if (n > 25600)
+    return fail(FFWD_ERR_UNSUPPORTED, "predictor_forward_block: n=%d > 25600 rows", n);
+  if (!x || !query || !w1 || !w2 || !scores || !workspace)
+    return fail(FFWD_ERR_VALIDATION, "predictor_forward_block: null pointer");
+  if (workspace_bytes < ffwd_predictor_workspace_bytes(1, d, r, f))
+    return fail(FFWD_ERR_VALIDATION, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carve c(workspace);
+  Pred p = carve_pred(c, 1, d, r, f, false);
+  const float sqrt_d = static_cast<float>(std::sqrt(static_cast<double>(d)));  // predictor.py:76
+  FFWD_CUDA(launch_pool_generic(x, x_is_f32 != 0, n, d, n, 0, 1, query, sqrt_d, p.pooled, s),
+            "pool");
+  FFWD_CUDA(launch_gemm_f64acc(p.pooled, w1, p.hidden, 1, d, r, true, p.partial, s), "w1");
+  FFWD_CUDA(launch_gemm_f64acc(p.hidden, w2, scores, 1, r, f, false, p.partial, s), "w2");
+  return FFWD_OK;
 }
 
 int ffwd_predictor_logits(const void* x, int x_is_f32, int T, int d, const float* query,
@@ -377,6 +413,10 @@ int ffwd_topk(const float* scores, int n_rows, int f, int k, int tp_rank, int tp
   if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size)
     return fail(FFWD_ERR_VALIDATION, "bad tensor-parallel rank %d of %d", tp_rank, tp_size);
   if (idx_global && ld_global < k) return fail(FFWD_ERR_VALIDATION, "ld_global < k");
+  if (n_rows > 0 && (!scores || (!idx_global && !idx_local)))
+    return fail(FFWD_ERR_VALIDATION, "topk: null scores or no index output");
+  if (idx_local && ld_local < std::min(k, (f + tp_size - 1) / tp_size))
+    return fail(FFWD_ERR_VALIDATION, "ld_local too small");
   FFWD_CUDA(launch_topk(scores, n_rows, f, k, tp_rank, tp_size, idx_global, ld_global, idx_local,
                         ld_local, counts, static_cast<cudaStream_t>(stream)),
             "topk");
@@ -414,6 +454,9 @@ int ffwd_sparse_ffn(const void* x_bf16, int T, int d, const void* wgu_t, const v
   if (rc) return rc;
   if ((rc = check_gemm_shapes(d, f_local))) return rc;
   if (has_comp && rc_local < 1) return fail(FFWD_ERR_VALIDATION, "compensator width must be >= 1");
+  if (!x_bf16 || !wgu_t || !wd || !y || !workspace)
+    return fail(FFWD_ERR_VALIDATION, "sparse_ffn: null pointer");
+  if (idx && ld_idx < k) return fail(FFWD_ERR_VALIDATION, "ld_idx < k");
   if (workspace_bytes < ffwd_sparse_ffn_workspace_bytes(T, d, f_local, rc_local, k))
     return fail(FFWD_ERR_VALIDATION, "workspace too small");
   Carve c(workspace);
@@ -480,12 +523,16 @@ int ffwd_ffn_layer2(const void* x_bf16, int T, int d, const void* wgu_t, const v
   if (has_comp && rc_local < 1) return fail(FFWD_ERR_VALIDATION, "compensator width must be >= 1");
   if ((residual || x_next_bf16) && tp_size != 1)
     return fail(FFWD_ERR_VALIDATION, "fused residual needs tp_size == 1 (all-reduce first)");
+  if (!x_bf16 || !wgu_t || !wd || !y || !workspace)
+    return fail(FFWD_ERR_VALIDATION, "ffn_layer: null x, weight, output or workspace pointer");
   if (workspace_bytes <
       ffwd_layer_workspace_bytes(T, d, f_global, f_local, rc_local, r, k, dense_first_last, tp_size))
     return fail(FFWD_ERR_VALIDATION, "workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int b0, nb;
   layer_split(T, k, f_global, dense_first_last, &b0, &nb);
+  if (nb > 0 && (!query || !w1 || !w2))
+    return fail(FFWD_ERR_VALIDATION, "ffn_layer: predicted blocks need the predictor weights");
   const int kmax = local_kmax(k, f_local);
   Carve c(workspace);
   Pred p = carve_pred(c, nb, d, r, f_global, true);
@@ -534,6 +581,8 @@ int ffwd_hidden_scores(const void* x_bf16, int T, int d, const void* wgu_t, int 
   int rc = check_common(T, d, f, f);
   if (rc) return rc;
   if ((rc = check_gemm_shapes(d, f))) return rc;
+  if (!x_bf16 || !wgu_t || !scores || !workspace)
+    return fail(FFWD_ERR_VALIDATION, "hidden_scores: null pointer");
   if (workspace_bytes < ffwd_hidden_scores_workspace_bytes(T, d, f))
     return fail(FFWD_ERR_VALIDATION, "workspace too small");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -543,7 +592,8 @@ int ffwd_hidden_scores(const void* x_bf16, int T, int d, const void* wgu_t, int 
   rc = run_ffn(x_bf16, T, d, wgu_t, nullptr, f, rc_local, w, nullptr, 0, 0, 0, nullptr, f, 0, 0,
                nullptr, nullptr, nullptr, s, /*up_only=*/true);
   if (rc) return rc;
-  FFWD_CUDA(launch_hidden_scores(w.h, false, w.hcols, T, f, scores, s), "hidden_scores");
+  FFWD_CUDA(launch_hidden_scores(w.h, false, w.hcols, T, f, kBlockTokens, scores, s),
+            "hidden_scores");
   return FFWD_OK;
 }
 
@@ -552,7 +602,9 @@ int ffwd_column_norms(const void* h, int is_f32, int n_rows, int ld, int f, floa
   g_err.clear();
   if (n_rows < 1 || f < 1 || ld < f)
     return fail(FFWD_ERR_VALIDATION, "column_norms dims n=%d f=%d ld=%d", n_rows, f, ld);
-  FFWD_CUDA(launch_hidden_scores(h, is_f32 != 0, ld, n_rows, f, scores,
+  if (!h || !scores) return fail(FFWD_ERR_VALIDATION, "column_norms: null pointer");
+  // one block of all n_rows rows (sparse.py:94-97 scores whatever block it is given)
+  FFWD_CUDA(launch_hidden_scores(h, is_f32 != 0, ld, n_rows, f, n_rows, scores,
                                  static_cast<cudaStream_t>(stream)),
             "column_norms");
   return FFWD_OK;
@@ -589,6 +641,8 @@ int ffwd_ffn_layer_mode(const void* x_bf16, int T, int d, const void* wgu_t, con
   if (dense_first_last != 0 && dense_first_last != 1)
     return fail(FFWD_ERR_VALIDATION, "ablation modes take dense_first_last 0 or 1");
   if (has_comp && rc_local < 1) return fail(FFWD_ERR_VALIDATION, "compensator width must be >= 1");
+  if (!x_bf16 || !wgu_t || !wd || !y || !workspace)
+    return fail(FFWD_ERR_VALIDATION, "ffn_layer_mode: null pointer");
   if (workspace_bytes <
       ffwd_ffn_layer_mode_workspace_bytes(T, d, f, rc_local, k, mode, dense_first_last))
     return fail(FFWD_ERR_VALIDATION, "workspace too small");
@@ -725,6 +779,8 @@ int ffwd_ffn_layer_tp_overlap(const void* x_bf16, int T, int d, const void* wgu_
   if (!partials || !outs || !flags || !y_done || !residual)
     return fail(FFWD_ERR_VALIDATION,
                 "overlapped completion needs partial, out, flag, y_done and residual pointers");
+  if (!x_bf16 || !wgu_t || !wd || !workspace)
+    return fail(FFWD_ERR_VALIDATION, "ffn_layer_tp_overlap: null x, weight or workspace pointer");
   for (int p = 0; p < tp_size; ++p)
     if (!partials[p] || !outs[p] || !flags[p] || !y_done[p] || (xnexts && !xnexts[p]))
       return fail(FFWD_ERR_VALIDATION, "null peer pointer for rank %d", p);
@@ -830,6 +886,7 @@ int ffwd_rope(void* qk, int is_f32, int T, int row_stride, int k_col, int n_head
     return fail(FFWD_ERR_VALIDATION, "rope layout: row_stride=%d k_col=%d for %d x %d", row_stride,
                 k_col, n_heads, d_head);
   if (pos0 < 0) return fail(FFWD_ERR_VALIDATION, "rope pos0=%d < 0", pos0);
+  if (!qk || !cos_t || !sin_t) return fail(FFWD_ERR_VALIDATION, "rope: null pointer");
   FFWD_CUDA(launch_rope(qk, is_f32 != 0, T, row_stride, k_col, n_heads, d_head, cos_t, sin_t,
                         cos32, sin32, pos0, static_cast<cudaStream_t>(stream)),
             "rope");
@@ -848,7 +905,12 @@ int ffwd_timing_read(double* ms_out, int* count_out, int n_stages) {
     if (count_out) count_out[i] = 0;
   }
   int rc = FFWD_OK;
-  for (const Rec& r : g_recs) {
+  std::vector<Rec> recs;
+  {
+    std::lock_guard<std::mutex> lk(g_rec_mu);
+    recs.swap(g_recs);
+  }
+  for (const Rec& r : recs) {
     float ms = 0.f;
     cudaError_t e = cudaEventSynchronize(r.b);
     if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, r.a, r.b);
@@ -857,10 +919,10 @@ int ffwd_timing_read(double* ms_out, int* count_out, int n_stages) {
       if (ms_out) ms_out[r.stage] += ms;
       if (count_out) count_out[r.stage] += r.kernels;
     }
+    std::lock_guard<std::mutex> lk(g_rec_mu);
     g_event_pool.push_back(r.a);
     g_event_pool.push_back(r.b);
   }
-  g_recs.clear();
   return rc;
 }
 

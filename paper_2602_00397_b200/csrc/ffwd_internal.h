@@ -46,6 +46,10 @@ struct PlanCounts {
 cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begin,
                         int blk_count, const float* query, float sqrt_d, float* logits,
                         float* pooled, const float* logits_in, cudaStream_t s);
+// Any-shape pooling: blocks of `rpb` rows, any d (the drop-in's small shapes).
+cudaError_t launch_pool_generic(const void* x, bool x_is_f32, int T, int d, int rpb,
+                                int blk_begin, int blk_count, const float* query, float sqrt_d,
+                                float* pooled, cudaStream_t s);
 // First pass alone: logits[t] for rows [tok0, tok0 + ntok) of x.
 cudaError_t launch_logits_only(const void* x, bool x_is_f32, int d, int tok0, int ntok,
                                const float* query, float sqrt_d, float* logits, cudaStream_t s);
@@ -69,8 +73,9 @@ cudaError_t launch_allreduce_overlap(const float* const* partial, float* const* 
                                      const float* residual, int T, int d, unsigned epoch,
                                      unsigned target, int sparse_begin, int sparse_count,
                                      int max_ctas, cudaStream_t s);
-// sparse.hidden_column_scores over bf16 H [n_blk*128 x hcols] -> scores [n_blk x f]
-cudaError_t launch_hidden_scores(const void* h, bool is_f32, int ld, int T, int f,
+// sparse.hidden_column_scores over H [T x ld] (bf16 or f32) in blocks of `rpb` rows ->
+// scores [ceil(T / rpb) x f]
+cudaError_t launch_hidden_scores(const void* h, bool is_f32, int ld, int T, int f, int rpb,
                                  float* scores, cudaStream_t s);
 cudaError_t launch_rope(void* qk, bool is_f32, int T, int row_stride, int k_col, int n_heads,
                         int d_head, const double* cos_t, const double* sin_t, const float* cos32,

@@ -293,12 +293,12 @@ namespace {
 
 template <typename E>
 __global__ void __launch_bounds__(256)
-    hidden_scores_kernel(const E* __restrict__ h, int ld, int T, int f,
+    hidden_scores_kernel(const E* __restrict__ h, int ld, int T, int f, int rpb,
                          float* __restrict__ scores) {
   const int b = blockIdx.y;
   const int j = blockIdx.x * 256 + threadIdx.x;
   if (j >= f) return;
-  const int t0 = b * kBlockTokens, n = min(kBlockTokens, T - t0);
+  const int t0 = b * rpb, n = min(rpb, T - t0);
   const E* col = h + static_cast<size_t>(t0) * ld + j;
   double s = 0.0;
 #pragma unroll 8
@@ -313,17 +313,18 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace
 
-cudaError_t launch_hidden_scores(const void* h, bool is_f32, int ld, int T, int f,
+cudaError_t launch_hidden_scores(const void* h, bool is_f32, int ld, int T, int f, int rpb,
                                  float* scores, cudaStream_t s) {
-  const int n_blk = (T + kBlockTokens - 1) / kBlockTokens;
+  if (rpb <= 0) return cudaErrorInvalidValue;
+  const int n_blk = (T + rpb - 1) / rpb;
   if (n_blk <= 0 || f <= 0) return cudaSuccess;
   const dim3 grid((f + 255) / 256, n_blk);
   if (is_f32)
-    hidden_scores_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(h), ld, T, f,
+    hidden_scores_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(h), ld, T, f, rpb,
                                                      scores);
   else
     hidden_scores_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(h), ld, T, f, scores);
+        static_cast<const __nv_bfloat16*>(h), ld, T, f, rpb, scores);
   return cudaGetLastError();
 }
 

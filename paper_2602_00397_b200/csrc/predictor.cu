@@ -250,6 +250,64 @@ __global__ void __launch_bounds__(kPoolThreads, FFWD_POOL_MINB)
   }
 }
 
+// Any-shape pooling (predictor.py:68-78 for blocks of `rpb` rows and any d): the drop-in's
+// path for shapes the streaming passes above do not take (d % 8 != 0, or one block of
+// n > 128 rows).  One CTA per block: per-row logits (warp per row, f64), the f64 softmax
+// over the block's n logits (kept in shared memory as f64), then pooled columns with one
+// f64 accumulator per thread.  Small shapes only; the prompt path uses the passes above.
+template <bool kF32>
+__global__ void __launch_bounds__(256)
+    pool_generic_kernel(const void* __restrict__ x, int T, int d, int rpb, int blk_begin,
+                        const float* __restrict__ query, float sqrt_d,
+                        float* __restrict__ pooled) {
+  extern __shared__ double sp[];  // [rpb] logits, then probabilities
+  __shared__ double wred[32];
+  pdl_wait();
+  pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const long long r0 = static_cast<long long>(blk_begin + blockIdx.x) * rpb;
+  const int n = static_cast<int>(min(static_cast<long long>(rpb), T - r0));
+  auto xat = [&](long long row, int c) -> double {
+    const size_t o = static_cast<size_t>(row) * d + c;
+    if constexpr (kF32) return static_cast<double>(__ldg(static_cast<const float*>(x) + o));
+    else return static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(x)[o]));
+  };
+  for (int t = warp; t < n; t += nw) {
+    double a = 0.0;
+    for (int c = lane; c < d; c += 32) a = fma(static_cast<double>(__ldg(query + c)), xat(r0 + t, c), a);
+    a = warp_sum_f64(a);
+    if (lane == 0) sp[t] = static_cast<double>(__fdiv_rn(static_cast<float>(a), sqrt_d));
+  }
+  __syncthreads();
+  double m = -INFINITY;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) m = fmax(m, sp[t]);
+  m = warp_max_f64(m);
+  if (lane == 0) wred[warp] = m;
+  __syncthreads();
+  m = wred[0];
+  for (int w = 1; w < nw; ++w) m = fmax(m, wred[w]);
+  __syncthreads();
+  double ssum = 0.0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) {
+    const double e = exp(sp[t] - m);
+    sp[t] = e;
+    ssum += e;
+  }
+  ssum = warp_sum_f64(ssum);
+  if (lane == 0) wred[warp] = ssum;
+  __syncthreads();
+  double sum = 0.0;
+  for (int w = 0; w < nw; ++w) sum += wred[w];
+  for (int t = threadIdx.x; t < n; t += blockDim.x)
+    sp[t] = static_cast<double>(static_cast<float>(sp[t] / sum));  // f32 probabilities
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    double acc = 0.0;
+    for (int t = 0; t < n; ++t) acc = fma(sp[t], xat(r0 + t, c), acc);
+    pooled[static_cast<size_t>(blockIdx.x) * d + c] = static_cast<float>(acc);
+  }
+}
+
 // ------------------------------------------------------------------ f64 GEMM
 // C[M x N] = f32(A[M x K] . B[K x N]) (then relu), f32 row-major operands, f64
 // accumulation on DMMA m8n8k4.  CTA tile 128 x BN, 4 warps (warp w: rows
@@ -531,6 +589,23 @@ cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begi
                     blk_count, lg, pooled);
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_pool_generic(const void* x, bool x_is_f32, int T, int d, int rpb,
+                                int blk_begin, int blk_count, const float* query, float sqrt_d,
+                                float* pooled, cudaStream_t s) {
+  if (blk_count <= 0) return cudaSuccess;
+  const size_t smem = static_cast<size_t>(rpb) * sizeof(double);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  static std::atomic<uint64_t> a32{0}, a16{0};
+  cudaError_t e = x_is_f32 ? ensure_smem_limit(pool_generic_kernel<true>, 200 * 1024, a32)
+                           : ensure_smem_limit(pool_generic_kernel<false>, 200 * 1024, a16);
+  if (e != cudaSuccess) return e;
+  if (x_is_f32)
+    return launch_k(pool_generic_kernel<true>, dim3(blk_count), dim3(256), smem, s, 1, x, T, d,
+                    rpb, blk_begin, query, sqrt_d, pooled);
+  return launch_k(pool_generic_kernel<false>, dim3(blk_count), dim3(256), smem, s, 1, x, T, d,
+                  rpb, blk_begin, query, sqrt_d, pooled);
 }
 
 cudaError_t launch_logits_only(const void* x, bool x_is_f32, int d, int tok0, int ntok,

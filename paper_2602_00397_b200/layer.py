@@ -16,7 +16,6 @@ bf16 layout the kernels gather from (see include/ffwd_b200.h).
 
 from __future__ import annotations
 
-from collections import OrderedDict
 from dataclasses import dataclass
 
 import numpy as np
@@ -24,7 +23,7 @@ import torch
 
 from . import _dev, _lib
 from .compensator import CompensatorParams
-from .errors import ValidationError
+from .errors import UnsupportedError, ValidationError
 from .predictor import DevicePredictor
 
 BLOCK = 128
@@ -50,7 +49,11 @@ def shard_comp_cols(rc: int, tp_rank: int, tp_size: int) -> tuple[int, int]:
 
 @dataclass
 class PackedLayer:
-    """One rank's FFN (+ compensator) weights in the kernels' neuron-major layout."""
+    """One rank's FFN (+ compensator) weights in the kernels' neuron-major layout.
+
+    ``d`` is the packed row width: d_model rounded up to 64 (the GEMMs' 128 B swizzle
+    atom) with zero columns, which leave every product unchanged; ``d_model`` is the
+    model's own width, to which inputs are padded and outputs sliced."""
     wgu_t: torch.Tensor   # bf16 [(2 f_local + roundup(rc_local, 256)) x d]
     wd: torch.Tensor      # bf16 [(f_local + roundup(rc_local, 64)) x d]
     d: int
@@ -59,6 +62,11 @@ class PackedLayer:
     rc_local: int
     tp_rank: int = 0
     tp_size: int = 1
+    d_model: int = 0
+
+    def __post_init__(self):
+        if not self.d_model:
+            self.d_model = self.d
 
     @property
     def device(self) -> torch.device:
@@ -96,40 +104,53 @@ def pack_layer(w_gate, w_up, w_down, comp: CompensatorParams | None = None, devi
         c1, c2 = c1[:, lo:hi], c2[lo:hi]
         rc_l = hi - lo
     bf = torch.bfloat16
-    wgu = torch.zeros((2 * f_l + _rup(rc_l, 256), d), dtype=bf, device=dev)
-    wgu[:f_l] = g[:, nid].t().to(dev, bf)
-    wgu[f_l:2 * f_l] = u[:, nid].t().to(dev, bf)
-    wd = torch.zeros((f_l + _rup(rc_l, 64), d), dtype=bf, device=dev)
-    wd[:f_l] = dn[nid].to(dev, bf)
+    dp = _rup(d, 64)  # zero columns: the K2 contraction and K3's extra outputs ignore them
+    nid_d = nid.to(dev) if g.is_cuda else nid
+    wgu = torch.zeros((2 * f_l + _rup(rc_l, 256), dp), dtype=bf, device=dev)
+    wgu[:f_l, :d] = g[:, nid_d].t().to(dev, bf)
+    wgu[f_l:2 * f_l, :d] = u[:, nid_d].t().to(dev, bf)
+    wd = torch.zeros((f_l + _rup(rc_l, 64), dp), dtype=bf, device=dev)
+    wd[:f_l, :d] = dn[nid_d].to(dev, bf)
     if rc_l:
-        wgu[2 * f_l:2 * f_l + rc_l] = c1.t().to(dev, bf)
-        wd[f_l:f_l + rc_l] = c2.to(dev, bf)
-    return PackedLayer(wgu_t=wgu, wd=wd, d=d, f_global=f, f_local=f_l, rc_local=rc_l,
-                       tp_rank=tp_rank, tp_size=tp_size)
-
-
-_pack_cache: "OrderedDict[tuple, tuple]" = OrderedDict()
+        wgu[2 * f_l:2 * f_l + rc_l, :d] = c1.t().to(dev, bf)
+        wd[f_l:f_l + rc_l, :d] = c2.to(dev, bf)
+    return PackedLayer(wgu_t=wgu, wd=wd, d=dp, f_global=f, f_local=f_l, rc_local=rc_l,
+                       tp_rank=tp_rank, tp_size=tp_size, d_model=d)
 
 
 def packed_for(lw, comp, device) -> PackedLayer:
-    """Packed weights for reference-style (numpy) layer weights, cached per object."""
-    key = (id(lw.w_gate), id(lw.w_up), id(lw.w_down), id(comp) if comp is not None else 0,
-           str(device))
-    hit = _pack_cache.get(key)
-    if hit is not None:
-        _pack_cache.move_to_end(key)
-        return hit[0]
-    p = pack_layer(lw.w_gate, lw.w_up, lw.w_down, comp, device=device)
-    _pack_cache[key] = (p, lw, comp)  # keep the sources alive so ids stay unique
-    while len(_pack_cache) > 4:
-        _pack_cache.popitem(last=False)
-    return p
+    """Packed weights for reference-style layer weights, kept resident on the weights'
+    own object (``_dev.cached_on``): the reference engine calls the drop-ins once per
+    (block, layer) (``engine.py:263``), so a layer is packed once, not once per call.  The
+    cache key is a fingerprint of the weight arrays (address, shape, torch version counter
+    or a content sample), so replaced weights repack; see ``invalidate_packed``."""
+    dev = torch.device(device)
+    key = (str(dev),) + _dev.fingerprint(lw.w_gate, lw.w_up, lw.w_down,
+                                         comp.w1 if comp is not None else None,
+                                         comp.w2 if comp is not None else None)
+    return _dev.cached_on(lw, "_ffwd_packed" if comp is None else "_ffwd_packed_comp", key,
+                          lambda: pack_layer(lw.w_gate, lw.w_up, lw.w_down, comp, device=dev))
+
+
+def invalidate_packed(obj) -> None:
+    """Drop the device copies cached on a weights object (after editing it in place)."""
+    store = getattr(obj, "__dict__", {})
+    for slot in [k for k in store if k.startswith("_ffwd_")]:
+        del store[slot]
 
 
 def _x_bf16(x, dev) -> torch.Tensor:
     if isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.bfloat16:
         return x.contiguous()
     return _dev.to_device(x, torch.bfloat16, dev)
+
+
+def _pad_cols(xb: torch.Tensor, width: int) -> torch.Tensor:
+    if xb.shape[1] == width:
+        return xb
+    out = torch.zeros((xb.shape[0], width), dtype=xb.dtype, device=xb.device)
+    out[:, :xb.shape[1]] = xb
+    return out
 
 
 def run_sparse_ffn(x, packed: PackedLayer, idx: torch.Tensor | None, k: int,
@@ -142,11 +163,17 @@ def run_sparse_ffn(x, packed: PackedLayer, idx: torch.Tensor | None, k: int,
     """
     dev = packed.device
     xb = _x_bf16(x, dev)
-    if xb.dim() != 2 or xb.shape[1] != packed.d:
-        raise ValidationError(f"FFN input shape {tuple(xb.shape)}, d_model={packed.d}")
+    if xb.dim() != 2 or xb.shape[1] != packed.d_model:
+        raise ValidationError(f"FFN input shape {tuple(xb.shape)}, d_model={packed.d_model}")
     T = xb.shape[0]
+    padded = packed.d != packed.d_model  # any d_model: zero columns up to the packed width
+    xb = _pad_cols(xb, packed.d)
     lib = _dev.lib_for(dev)
-    y = out if out is not None else torch.empty((T, packed.d), dtype=torch.float32, device=dev)
+    if padded:
+        y = torch.empty((T, packed.d), dtype=torch.float32, device=dev)
+    else:
+        y = out if out is not None else torch.empty((T, packed.d), dtype=torch.float32,
+                                                    device=dev)
     kk = packed.f_local if idx is None else k
     ws_n = lib.ffwd_sparse_ffn_workspace_bytes(T, packed.d, packed.f_local, packed.rc_local, kk)
     ws = _dev.workspace(dev, ws_n)
@@ -156,6 +183,12 @@ def run_sparse_ffn(x, packed: PackedLayer, idx: torch.Tensor | None, k: int,
         packed.f_local, packed.rc_local, _dev.ptr(idx), int(idx_per_block), ld,
         _dev.ptr(counts), kk, int(has_comp and packed.rc_local > 0), y.data_ptr(),
         ws.data_ptr(), ws.numel(), _dev.stream_handle(dev)), "sparse_ffn")
+    if padded:
+        y = y[:, :packed.d_model]
+        if out is not None:
+            out.copy_(y)
+            return out
+        return y.contiguous()
     return y
 
 
@@ -227,6 +260,9 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
     (``norm.rmsnorm(..., predictor=...)``), which skips the pooling's first pass.
     """
     dev = packed.device
+    if packed.d != packed.d_model:
+        raise UnsupportedError(f"sparse_ffn_layer needs d_model % 64 == 0 (got {packed.d_model}); "
+                               "the per-block drop-ins take any width")
     xb = _x_bf16(x, dev)
     T, d = xb.shape
     if d != packed.d or predictor.d != d or predictor.f != packed.f_global:
@@ -279,8 +315,10 @@ def oracle_scores(x, packed: PackedLayer) -> torch.Tensor:
     dev = packed.device
     xb = _x_bf16(x, dev)
     T, d = xb.shape
-    if d != packed.d:
-        raise ValidationError(f"x width {d} != d_model {packed.d}")
+    if d != packed.d_model:
+        raise ValidationError(f"x width {d} != d_model {packed.d_model}")
+    xb = _pad_cols(xb, packed.d)
+    d = packed.d
     lib = _dev.lib_for(dev)
     f = packed.f_local
     n_blk = -(-T // BLOCK)
@@ -308,6 +346,8 @@ def ffn_layer_mode(x, packed: PackedLayer, k: int, mode: str, dense_first_last: 
         raise ValidationError(f"unknown mode {mode!r}; expected one of {tuple(_MODE_CODE)}")
     if packed.tp_size != 1:
         raise ValidationError("the ablation modes need the unsharded layer (tp_size 1)")
+    if packed.d != packed.d_model:
+        raise UnsupportedError(f"ffn_layer_mode needs d_model % 64 == 0 (got {packed.d_model})")
     dev = packed.device
     xb = _x_bf16(x, dev)
     T, d = xb.shape

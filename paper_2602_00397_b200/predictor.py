@@ -141,17 +141,25 @@ def predictor_forward(params, x):
     tensor); the arithmetic runs on the GPU either way.
     """
     host = _dev.is_host(x)
-    if host:
-        xa = np.asarray(x)
-        if xa.ndim != 2 or xa.shape[1] != params.query.shape[1]:
-            raise ValidationError(
-                f"predictor input shape {xa.shape}, d_model={params.query.shape[1]}")
+    d = params.w1.shape[0]
+    shape = tuple(np.asarray(x).shape) if host else tuple(x.shape)
+    if len(shape) != 2 or shape[1] != d or shape[0] < 1:
+        raise ValidationError(f"predictor input shape {shape}, d_model={d}")
     dev = _dev.device_of(x, getattr(params, "w1", None))
-    dp = params if isinstance(params, DevicePredictor) else DevicePredictor.from_params(params, dev)
+    if isinstance(params, DevicePredictor):
+        dp = params
+    else:  # resident across calls (engine.py:286 calls this once per block and layer)
+        key = (str(dev),) + _dev.fingerprint(params.query, params.w1, params.w2)
+        dp = _dev.cached_on(params, "_ffwd_device", key,
+                            lambda: DevicePredictor.from_params(params, dev))
     xt = _dev.to_device(x, torch.float32, dev) if host or x.dtype not in (
-        torch.float32, torch.bfloat16) else x
-    n = xt.shape[0]
-    if n > 128:
-        raise ValidationError(f"predictor_forward scores one block (<= 128 rows), got {n}")
-    s = predictor_scores(dp, xt, 0, 1)[0]
+        torch.float32, torch.bfloat16) else x.contiguous()
+    # one block of any n rows and any width (the reference pools whatever it is handed)
+    lib = _dev.lib_for(dev)
+    s = torch.empty((dp.f,), dtype=torch.float32, device=dev)
+    ws = _dev.workspace(dev, lib.ffwd_predictor_workspace_bytes(1, dp.d, dp.r, dp.f))
+    _lib.check(lib.ffwd_predictor_forward_block(
+        xt.data_ptr(), int(xt.dtype == torch.float32), xt.shape[0], dp.d, dp.query.data_ptr(),
+        dp.w1.data_ptr(), dp.w2.data_ptr(), dp.r, dp.f, s.data_ptr(), ws.data_ptr(), ws.numel(),
+        _dev.stream_handle(dev)), "predictor_forward")
     return _dev.to_host_f32(s) if host else s

@@ -153,8 +153,8 @@ def hidden_column_scores(hidden):
     if h.dim() != 2:
         raise ValidationError(f"hidden must be 2-D, got shape {tuple(h.shape)}")
     n, f = h.shape
-    if n > 128:
-        raise ValidationError(f"one block of at most 128 tokens, got {n}")
+    if n < 1:
+        raise ValidationError("hidden must hold at least one row")
     out = torch.empty((1, f), dtype=torch.float32, device=dev)
     lib = _dev.lib_for(dev)
     _lib.check(lib.ffwd_column_norms(h.data_ptr(), int(h.dtype == torch.float32), n, f, f,

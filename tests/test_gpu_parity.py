@@ -215,10 +215,20 @@ def test_errors_map_to_reference_types(ff):
         ff.sparse_ffn_layer(x, packed, dp, c["f"] + 1)
     with pytest.raises(ff.ValidationError):
         ff.topk_indices(np.ones(3, np.float32), 4)
-    g = np.zeros((96, 200), np.float32)
-    p96 = ff.pack_layer(g, g, g.T.copy(), None, device="cuda")
+    # any d_model works on the per-block drop-ins (zero-padded to the 64-column atom) ...
+    rng = np.random.default_rng(96)
+    w = {n_: orc.bf16_round(rng.standard_normal(s_).astype(np.float32) * np.float32(0.1))
+         for n_, s_ in (("g", (96, 200)), ("u", (96, 200)), ("dn", (200, 96)))}
+    p96 = ff.pack_layer(w["g"], w["u"], w["dn"], None, device="cuda")
+    x96 = orc.bf16_round(rng.standard_normal((128, 96)).astype(np.float32))
+    got = ff.dense_ffn(torch.from_numpy(x96).cuda(), p96).cpu().numpy()
+    assert got.shape == (128, 96)
+    assert_close(got, orc.dense_ffn(x96, w["g"], w["u"], w["dn"]), "d=96 dense drop-in")
+    # ... but the layer-batched hot path keeps the kernels' native width
+    dp96 = ff.DevicePredictor.from_params(
+        ff.PredictorParams(**orc.init_predictor(rng, 96, 200)), "cuda")
     with pytest.raises(ff.UnsupportedError):
-        ff.dense_ffn(torch.zeros((128, 96), device="cuda"), p96)
+        ff.sparse_ffn_layer(torch.zeros((128, 96), device="cuda"), p96, dp96, 100)
 
 
 @pytest.mark.parametrize("shape", [("l8b", 4096, 14336), ("qwen8b", 4096, 12288)])
