@@ -409,6 +409,60 @@ def measure_ttft(layers, cfg_name: str, dev, steps: int) -> dict:
                      f"{steps} prefills per mode (modes alternated) after 2 warm-ups each"}
 
 
+# ------------------------------------------------------------------ other splits (N > 1)
+def time_other_splits(args, rank: int, world: int, dev, timed, skip: str) -> dict:
+    """The two splits besides the headline's, timed on the same GPUs for the extra keys:
+    sequence parallel (the prompt's 128-token blocks split across ranks, weights
+    replicated, no data-path collective: the FFN branch is block-local, engine.py:254-310)
+    and data parallel (one independent prompt per rank, BASELINE configs[4])."""
+    import paper_2602_00397_b200 as ff
+    from paper_2602_00397_b200 import layer as fl
+    from paper_2602_00397_b200.norm import rmsnorm
+    d, f, L, T, keep = CONFIGS[args.config]
+    layers, _ = make_layers(args.config, dev, 0, 1)
+    n_blk = -(-T // 128)
+    gain = torch.ones(d, device=dev)
+    out = {}
+    for mode in ("sp", "dp"):
+        if mode == skip:
+            continue
+        gx = torch.Generator(device=dev)
+        gx.manual_seed(99 + (rank if mode == "dp" else 0))
+        x = torch.randn((T, d), generator=gx, device=dev).to(torch.bfloat16).float()
+        dfl = True
+        if mode == "sp":
+            b0, b1, dfl = fl.seq_shard(n_blk, rank, world)
+            x = x[b0 * 128:min(T, b1 * 128)].contiguous()
+        Tl = x.shape[0]
+        res = torch.empty_like(x)
+        xb = torch.empty((Tl, d), dtype=torch.bfloat16, device=dev)
+        lg = torch.empty((Tl,), dtype=torch.float32, device=dev)
+        ws = torch.empty(max(fl.layer_workspace_bytes(Tl, p, q.r, k, dfl) for p, q, k in layers),
+                         dtype=torch.uint8, device=dev)
+
+        def st():
+            res.copy_(x)
+            for packed, dp, k in layers:
+                rmsnorm(res, gain, out=xb, predictor=dp, logits=lg)
+                ff.sparse_ffn_layer(xb, packed, dp, k, out=res, residual=res, logits_in=lg,
+                                    workspace=ws, dense_first_last=dfl)
+
+        for _ in range(max(1, args.warmup)):
+            st()
+        ms = timed(st, args.steps)
+        prompts = world if mode == "dp" else 1
+        out[mode] = {"ms_per_layer": ms / L, "prompts_per_step": prompts,
+                     "prefill_ffn_tokens_per_s": prompts * T / (ms * 1e-3),
+                     "scaling": "weak" if mode == "dp" else "strong",
+                     "what": ("the prompt's 128-token blocks split over the ranks, weights "
+                              "replicated, no collective" if mode == "sp" else
+                              "one independent prompt per rank, no collective")}
+        del res, xb, lg, ws
+    del layers
+    torch.cuda.empty_cache()
+    return out
+
+
 # ------------------------------------------------------------------ GPU arm
 def run_gpu(args, rank: int, world: int) -> None:
     import paper_2602_00397_b200 as ff
@@ -428,6 +482,9 @@ def run_gpu(args, rank: int, world: int) -> None:
     # dp: every rank runs the whole stack on its own prompt (independent prompts, no
     # collective in the data path)
     tp = world if args.parallel == "tp" else 1
+    # tp + rs_ag (the default for N > 1): sequence-parallel residual stream, all-gather of
+    # the bf16 FFN input and reduce-scatter of the partial FFN output (tp.SeqParallelTP)
+    rs_ag = tp > 1 and args.collective == "rs_ag"
     layers, ks = make_layers(args.config, dev, rank if tp > 1 else 0, tp)
     n_blk = -(-T // 128)
     gx = torch.Generator(device=dev)
@@ -439,16 +496,27 @@ def run_gpu(args, rank: int, world: int) -> None:
     if args.parallel == "sp" and world > 1:
         blk0, blk1, dfl = fl.seq_shard(n_blk, rank, world)
         x0 = x0[blk0 * 128:min(T, blk1 * 128)].contiguous()
+    gain = torch.ones(d, device=dev)            # ffn_norm gains (ones, synthetic.py:41)
+    sp_tp = None
+    if rs_ag:
+        from paper_2602_00397_b200.tp import SeqParallelTP, TorchComm, seq_rows
+        r0, r1 = seq_rows(T, rank, world)
+        x0 = x0[r0:r1].contiguous()  # this rank's rows of the residual stream
+        sp_tp = SeqParallelTP(layers, T, d, rank, world, dev, comm=TorchComm(), gain=gain,
+                              reduce_dtype=torch.bfloat16 if args.reduce_dtype == "bf16"
+                              else torch.float32)
     T_loc = x0.shape[0]
     n_dense_loc = int(blk0 == 0) + int(blk1 == n_blk) if dfl != True else min(2, n_blk)  # noqa: E712
     n_pred_loc = (blk1 - blk0) - n_dense_loc
     res = torch.empty_like(x0)
     xb = torch.empty((T_loc, d), dtype=torch.bfloat16, device=dev)
-    ybuf = torch.empty_like(x0) if tp > 1 else None
-    ws_bytes = max(fl.layer_workspace_bytes(T_loc, p, dp.r, k, dfl) for p, dp, k in layers)
+    ybuf = torch.empty_like(x0) if tp > 1 and not rs_ag else None
+    ws_bytes = max(fl.layer_workspace_bytes(T if rs_ag else T_loc, p, dp.r, k, dfl)
+                   for p, dp, k in layers)
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    if sp_tp is not None:
+        sp_tp.workspace = ws
 
-    gain = torch.ones(d, device=dev)            # ffn_norm gains (ones, synthetic.py:41)
     lg = torch.empty((T_loc,), dtype=torch.float32, device=dev)
     peers = None
     if tp > 1 and args.collective in ("fused", "overlap"):
@@ -461,6 +529,9 @@ def run_gpu(args, rank: int, world: int) -> None:
         # engine.py:267-308 per layer: x = rmsnorm(h, ffn_norm) (fused with the predictor's
         # per-token logits), then predictor -> top-k -> sparse FFN + compensator, h += y
         res.copy_(x_src)
+        if sp_tp is not None:  # norm on T/N rows -> AG(x, logits) -> FFN shard -> RS(y)
+            sp_tp.stack(res)
+            return
         for packed, dp, k in layers:
             rmsnorm(res, gain, out=xb, predictor=dp, logits=lg)
             if tp == 1:
@@ -652,7 +723,12 @@ def run_gpu(args, rank: int, world: int) -> None:
         else "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init normal*0.02 weights, N(0,1) bf16 hidden states)",
         "config": workload_config(args, T, L, ks, world),
-        "collective": args.collective if tp > 1 else None,
+        "collective": ({"rs_ag": f"NCCL all-gather x (bf16) + reduce-scatter y "
+                                  f"({args.reduce_dtype}), sequence-parallel residual",
+                        "allreduce": "NCCL all-reduce of y (f32)", "nccl": "NCCL all-reduce "
+                        "of y (f32)", "fused": "peer-memory all-reduce kernel (NVLink P2P)",
+                        "overlap": "peer-memory all-reduce overlapped with the down "
+                                   "projection"}[args.collective] if tp > 1 else None),
         "l2": (f"inputs larger than L2 (residual stream {T_loc * d * 4 / 2**20:.0f} MiB f32, "
                f"{w_layer / 2**20:.0f} MiB bf16 weights per layer, {L} distinct layers per "
                "step); no flush"),
@@ -681,6 +757,12 @@ def run_gpu(args, rank: int, world: int) -> None:
         "predictor_f32_input": f32_variant,
     }
 
+    # ---- the other splits (N > 1): extra keys on the same line
+    if world > 1 and not args.skip_alt:
+        del layers
+        torch.cuda.empty_cache()
+        out["other_splits"] = time_other_splits(args, rank, world, dev, timed, args.parallel)
+        layers = None
     # ---- dense baselines on one layer (rank 0 only, single GPU)
     if world == 1 and not args.skip_dense:
         packed, dp, k = layers[0]
@@ -749,14 +831,21 @@ def main():
     ap.add_argument("--skip-ttft", action="store_true")
     ap.add_argument("--skip-f32-pred", action="store_true",
                     help="skip timing the f32-predictor-input variant")
-    ap.add_argument("--collective", default="nccl", choices=["nccl", "fused", "overlap"],
-                    help="TP completion: NCCL all-reduce, the fused peer-memory kernel, or "
-                         "that kernel overlapped with the down projection block by block")
-    ap.add_argument("--parallel", default="sp", choices=["sp", "tp", "dp"],
-                    help="N>1: sequence parallel (the prompt's 128-token blocks split "
-                         "across GPUs, weights replicated, no collective), tensor parallel "
-                         "over d_ffn (one all-reduce per layer), or data parallel (one "
-                         "prompt per GPU)")
+    ap.add_argument("--collective", default="rs_ag",
+                    choices=["rs_ag", "allreduce", "nccl", "fused", "overlap"],
+                    help="TP completion: rs_ag = sequence-parallel residual (NCCL all-gather "
+                         "of x, reduce-scatter of y; the default), allreduce (= nccl) = NCCL "
+                         "all-reduce of y, fused = the peer-memory all-reduce kernel, overlap "
+                         "= that kernel draining blocks while the down projection runs")
+    ap.add_argument("--reduce-dtype", default="f32", choices=["f32", "bf16"],
+                    help="rs_ag: dtype of the partial y reduce-scatter")
+    ap.add_argument("--parallel", default="tp", choices=["tp", "sp", "dp"],
+                    help="N>1: tensor parallel over d_ffn (the north star's split; default), "
+                         "sequence parallel (the prompt's 128-token blocks split across GPUs, "
+                         "weights replicated, no collective), or data parallel (one prompt "
+                         "per GPU)")
+    ap.add_argument("--skip-alt", action="store_true",
+                    help="N>1: skip timing the other two splits (sp, dp) for the extra keys")
     ap.add_argument("--raster", default="", help="UP,DOWN blocks per L2 raster group (tuning)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -767,6 +856,9 @@ def main():
     if world > 1:
         torch.cuda.set_device(local_device())
         if BACKEND == "nccl":  # bind the rank's GPU (barriers and collectives use it)
+            # communicator lines (rank / nRanks / transports) for the run's record
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             torch.distributed.init_process_group(
                 "nccl", device_id=torch.device("cuda", local_device()))
         else:

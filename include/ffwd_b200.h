@@ -57,6 +57,14 @@ FFWD_API int ffwd_device_check(int device);
 
 /* Tuning knobs of the gather-GEMM rasterisation (blocks per L2 group). */
 FFWD_API int ffwd_set_raster(int up_group, int down_group);
+/*
+ * Deadline of the cross-GPU waits of the peer-memory completions (ffwd_allreduce_residual,
+ * ffwd_ffn_layer_tp_overlap): a rank that waits longer than `ms` for a peer traps (the
+ * CUDA context reports an error) instead of hanging the GPU.  Default 60000 ms, so
+ * ordinary rank skew (first-iteration setup, a host-side pause) is waited out.
+ */
+FFWD_API int ffwd_set_spin_timeout_ms(int ms);
+
 /* Tuning knob: odd up-projection raster groups sweep their neuron tiles downwards (1,
  * default) so the previous group's last weight rows are still in L2. */
 FFWD_API int ffwd_set_serpentine(int on);

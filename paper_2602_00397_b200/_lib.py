@@ -26,6 +26,7 @@ SIGNATURES = {
     "ffwd_device_check": (_c_int, [_c_int]),
     "ffwd_set_raster": (_c_int, [_c_int, _c_int]),
     "ffwd_set_serpentine": (_c_int, [_c_int]),
+    "ffwd_set_spin_timeout_ms": (_c_int, [_c_int]),
     "ffwd_set_pdl": (_c_int, [_c_int]),
     "ffwd_predictor_workspace_bytes": (_c_size, [_c_int, _c_int, _c_int, _c_int]),
     "ffwd_predictor_forward": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp,

@@ -19,7 +19,9 @@
 //              flags_p[N + r] = epoch after all its stores; every CTA then waits for
 //              flags_r[N + q] >= epoch, so when the kernel retires on rank r every
 //              peer has finished writing rank r's output.
-// Spins are bounded (about a second) and trap instead of hanging the GPU.
+// Spins are bounded by a wall-clock deadline (%globaltimer; ffwd_set_spin_timeout_ms,
+// default 60 s, so ordinary rank skew -- first-iteration setup, a host pause -- is
+// waited out) and trap instead of hanging the GPU when a peer is really gone.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -42,7 +44,14 @@ struct ArArgs {
   const float* residual;            // this rank's residual (may alias out[rank])
   int n, rank, T, d;
   unsigned epoch;
+  unsigned long long timeout_ns;    // spin deadline per wait
 };
+
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   unsigned v;
@@ -54,12 +63,13 @@ __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ void wait_flags(const unsigned* f, int n, unsigned epoch) {
+__device__ __forceinline__ void wait_flags(const unsigned* f, int n, unsigned epoch,
+                                           unsigned long long timeout_ns) {
   for (int q = 0; q < n; ++q) {
-    long long spins = 0;
+    const unsigned long long t0 = gtimer_ns();
     while (static_cast<int>(ld_acquire_sys(f + q) - epoch) < 0) {
       __nanosleep(64);
-      if (++spins > (1ll << 24)) __trap();  // a peer never arrived: fail loudly
+      if (gtimer_ns() - t0 > timeout_ns) __trap();  // a peer never arrived: fail loudly
     }
   }
 }
@@ -137,7 +147,7 @@ __device__ __forceinline__ void depart(const ArArgs& a) {
   }
   __syncthreads();
   if (last && threadIdx.x < n) st_release_sys(a.flags[threadIdx.x] + n + r, a.epoch);
-  if (threadIdx.x == 0) wait_flags(a.flags[r] + n, n, a.epoch);
+  if (threadIdx.x == 0) wait_flags(a.flags[r] + n, n, a.epoch, a.timeout_ns);
   __syncthreads();
 }
 
@@ -148,7 +158,7 @@ __global__ void __launch_bounds__(kArThreads) allreduce_residual_kernel(ArArgs a
     __threadfence_system();
     st_release_sys(a.flags[threadIdx.x] + r, a.epoch);
   }
-  if (threadIdx.x == 0) wait_flags(a.flags[r], n, a.epoch);
+  if (threadIdx.x == 0) wait_flags(a.flags[r], n, a.epoch, a.timeout_ns);
   __syncthreads();
 
   // ---- reduce my row slice, fused residual add, all-gather stores
@@ -183,10 +193,10 @@ __global__ void __launch_bounds__(kArThreads) allreduce_overlap_kernel(ArOvArgs 
                                      : ov.sparse_begin + (o - n_dense);
     if (threadIdx.x == 0) {
       for (int q = 0; q < n; ++q) {
-        long long spins = 0;
+        const unsigned long long t0 = gtimer_ns();
         while (static_cast<int>(ld_acquire_sys(ov.ydone[q] + b) - ov.target) < 0) {
           __nanosleep(128);
-          if (++spins > (1ll << 24)) __trap();  // a rank's K3 never finished block b
+          if (gtimer_ns() - t0 > a.timeout_ns) __trap();  // a rank's K3 never finished block b
         }
       }
     }
@@ -219,6 +229,7 @@ cudaError_t launch_allreduce_residual(const float* const* partial, float* const*
   a.T = T;
   a.d = d;
   a.epoch = epoch;
+  a.timeout_ns = spin_timeout_ns();
   // every CTA spins at the end, so the grid must be co-resident: one wave
   allreduce_residual_kernel<<<max_ctas, kArThreads, 0, s>>>(a);
   return cudaGetLastError();
@@ -250,6 +261,7 @@ cudaError_t launch_allreduce_overlap(const float* const* partial, float* const* 
   a.T = T;
   a.d = d;
   a.epoch = epoch;
+  a.timeout_ns = spin_timeout_ns();
   ov.target = target;
   ov.sparse_begin = sparse_begin;
   ov.sparse_count = sparse_count;

@@ -38,6 +38,7 @@ std::atomic<int> g_blockdep{FFWD_BLOCKDEP_DEFAULT};
 std::atomic<int> g_pdl{FFWD_PDL_DEFAULT};
 // ncu sweep: K3 DRAM 3.0 GB -> 1.7 GB per layer vs 8 (profiles/r1_raster_sweep.txt)
 std::atomic<int> g_down_group{16};
+std::atomic<long long> g_spin_timeout_ms{60000};
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -304,6 +305,10 @@ int check_gemm_shapes(int d, int f_local) {
 
 namespace ffwd {
 bool pdl_enabled() { return g_pdl.load(std::memory_order_relaxed) != 0; }
+unsigned long long spin_timeout_ns() {
+  return static_cast<unsigned long long>(g_spin_timeout_ms.load(std::memory_order_relaxed)) *
+         1000000ull;
+}
 }  // namespace ffwd
 
 extern "C" {
@@ -324,6 +329,12 @@ int ffwd_device_check(int device) {
 
 int ffwd_set_pdl(int on) {
   g_pdl = on != 0;
+  return FFWD_OK;
+}
+
+int ffwd_set_spin_timeout_ms(int ms) {
+  if (ms < 1) return fail(FFWD_ERR_VALIDATION, "spin timeout must be >= 1 ms, got %d", ms);
+  g_spin_timeout_ms.store(ms);
   return FFWD_OK;
 }
 
@@ -521,10 +532,12 @@ int ffwd_ffn_layer2(const void* x_bf16, int T, int d, const void* wgu_t, const v
     return fail(FFWD_ERR_VALIDATION, "f_local=%d is not rank %d's strided share of d_ffn=%d",
                 f_local, tp_rank, f_global);
   if (has_comp && rc_local < 1) return fail(FFWD_ERR_VALIDATION, "compensator width must be >= 1");
-  if ((residual || x_next_bf16) && tp_size != 1)
-    return fail(FFWD_ERR_VALIDATION, "fused residual needs tp_size == 1 (all-reduce first)");
-  if (!x_bf16 || !wgu_t || !wd || !y || !workspace)
+  if (residual && tp_size != 1)
+    return fail(FFWD_ERR_VALIDATION, "fused residual needs tp_size == 1 (reduce the partials first)");
+  if (!x_bf16 || !wgu_t || !wd || !workspace || (!y && !x_next_bf16))
     return fail(FFWD_ERR_VALIDATION, "ffn_layer: null x, weight, output or workspace pointer");
+  if (!y && residual)
+    return fail(FFWD_ERR_VALIDATION, "ffn_layer: the residual add needs the f32 output y");
   if (workspace_bytes <
       ffwd_layer_workspace_bytes(T, d, f_global, f_local, rc_local, r, k, dense_first_last, tp_size))
     return fail(FFWD_ERR_VALIDATION, "workspace too small");

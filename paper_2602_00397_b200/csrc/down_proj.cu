@@ -262,11 +262,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               o[4 * j + 3] += r.w;
             }
           }
-          float4* dst = reinterpret_cast<float4*>(a.y + row_off + c);
+          if (a.y) {  // null: bf16 output only (a tensor-parallel partial for a bf16 reduce)
+            float4* dst = reinterpret_cast<float4*>(a.y + row_off + c);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 v4 = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
-            if (FFWD_K3_STREAM_EPI) __stcs(dst + j, v4); else dst[j] = v4;
+            for (int j = 0; j < 4; ++j) {
+              const float4 v4 = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+              if (FFWD_K3_STREAM_EPI) __stcs(dst + j, v4); else dst[j] = v4;
+            }
           }
           if (a.x_next) {  // next layer's bf16 input
             uint4* xn = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(a.x_next) +

@@ -58,6 +58,8 @@ cudaError_t launch_rmsnorm(float* x, const float* gain, int T, int d, double eps
                            const void* add, int add_kind, void* out_bf16, float* out_f32,
                            const float* query, float sqrt_d, float* logits, int logit_row0,
                            int logit_row1, bool logits_from_f32, cudaStream_t s);
+// Deadline of the cross-GPU spin waits (ffwd_set_spin_timeout_ms; default 60 s).
+unsigned long long spin_timeout_ns();
 // Fused tensor-parallel completion (allreduce.cu): out_p = residual + sum_q partial_q on
 // every rank p (peer pointers), optional bf16 copy; flags: per-rank [2n + 1] words.
 cudaError_t launch_allreduce_residual(const float* const* partial, float* const* out,

@@ -241,7 +241,7 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
                      workspace: torch.Tensor | None = None,
                      residual: torch.Tensor | None = None, x_next: torch.Tensor | None = None,
                      x_pred_f32: torch.Tensor | None = None,
-                     logits_in: torch.Tensor | None = None):
+                     logits_in: torch.Tensor | None = None, f32_out: bool = True):
     """One layer's FFN branch over every block of x (T, d); returns y (T, d) f32.
 
     Semantics of ``engine.py:254-310`` (mode "predicted"): blocks 0 and n-1 run
@@ -258,6 +258,8 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
     reference's f32 RMSNorm output) instead of x; ``logits_in`` (f32 (T,)) are
     per-token predictor logits already produced by the FFN-input producer
     (``norm.rmsnorm(..., predictor=...)``), which skips the pooling's first pass.
+    ``f32_out=False`` writes only the bf16 ``x_next`` (no f32 y; returned in its place):
+    a tensor-parallel partial for a bf16 reduce-scatter.
     """
     dev = packed.device
     if packed.d != packed.d_model:
@@ -271,7 +273,12 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
     if not 1 <= k <= packed.f_global:
         raise ValidationError(f"k={k} out of range [1, {packed.f_global}]")
     lib = _dev.lib_for(dev)
-    y = out if out is not None else torch.empty((T, d), dtype=torch.float32, device=dev)
+    if f32_out:
+        y = out if out is not None else torch.empty((T, d), dtype=torch.float32, device=dev)
+    else:
+        if x_next is None or residual is not None:
+            raise ValidationError("f32_out=False needs x_next (the bf16 output) and no residual")
+        y = None
     n_blk = -(-T // BLOCK)
     dfl = dense_first_last_code(dense_first_last)
     if k >= packed.f_global:
@@ -293,10 +300,12 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
         xb.data_ptr(), T, d, packed.wgu_t.data_ptr(), packed.wd.data_ptr(), packed.f_local,
         packed.rc_local, predictor.query.data_ptr(), predictor.w1.data_ptr(),
         predictor.w2.data_ptr(), predictor.r, predictor.f, k, dfl,
-        int(has_comp and packed.rc_local > 0), packed.tp_rank, packed.tp_size, y.data_ptr(),
+        int(has_comp and packed.rc_local > 0), packed.tp_rank, packed.tp_size, _dev.ptr(y),
         _dev.ptr(residual), _dev.ptr(x_next), _dev.ptr(idx), k if idx is not None else 0,
         _dev.ptr(x_pred_f32), _dev.ptr(logits_in), ws.data_ptr(), ws.numel(),
         _dev.stream_handle(dev)), "ffn_layer")
+    if y is None:
+        y = x_next
     if return_indices:
         return y, idx
     return y

@@ -256,3 +256,148 @@ class PeerBuffers:
         for p in self._opened:
             lib.ffwd_ipc_close(p)
         self._opened = []
+
+
+# ------------------------------------------------- sequence-parallel residual (RS / AG)
+class TorchComm:
+    """The two collectives of the sequence-parallel TP layer over ``torch.distributed``
+    (NCCL over NVLink on the GPU box; gloo for CPU tests)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        # gloo has no CUDA all-gather / reduce-scatter: stage through host memory (the
+        # single-GPU functional emulation of the bench; NCCL takes device tensors)
+        self.staged = dist.get_backend(group) == "gloo"
+
+    def _run(self, fn, out, inp):
+        if self.staged and out.is_cuda:
+            o, i = out.cpu(), inp.cpu()
+            if o.dtype == torch.bfloat16:  # gloo reductions of bf16: widen on the host
+                o, i = o.float(), i.float()
+            fn(o, i, group=self.group)
+            out.copy_(o)
+        else:
+            fn(out, inp, group=self.group)
+
+    def all_gather(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        self._run(dist.all_gather_into_tensor, out, inp)
+
+    def reduce_scatter(self, out: torch.Tensor, inp: torch.Tensor) -> None:
+        self._run(lambda o, i, group: dist.reduce_scatter_tensor(o, i, op=dist.ReduceOp.SUM,
+                                                                 group=group), out, inp)
+
+
+def seq_rows(T: int, rank: int, world: int) -> tuple[int, int]:
+    """Rows [r0, r1) of the residual stream rank `rank` owns (T % world == 0)."""
+    if T % world:
+        raise ValidationError(f"{T} tokens do not split evenly over {world} ranks")
+    n = T // world
+    return rank * n, (rank + 1) * n
+
+
+class SeqParallelTP:
+    """Tensor parallelism over d_ffn with a sequence-parallel residual stream.
+
+    The FFN branch of ``engine.py:263-308`` split over N ranks.  Rank r owns rows
+    [r T/N, (r+1) T/N) of the f32 residual stream h and the strided d_ffn shard
+    {j : j % N == r} of every layer (``pack_layer(..., tp_rank=r, tp_size=N)``).  Per layer:
+
+      1. ``norm``: h[R_r] += y[R_r] (the previous layer's reduced FFN output,
+         ``engine.py:308``) and x[R_r] = rmsnorm(h[R_r]) with the predictor's per-token
+         logits -- one kernel (``ffwd_rmsnorm_ex`` with ``add``) on T/N rows;
+      2. ``gather``: all-gather x (bf16 [T x d]) and the logits (f32 [T]);
+      3. ``ffn``: the FFN branch over all T tokens on this rank's shard: the replicated
+         predictor gives every rank the same global top-k (bit-exact), each keeps its own
+         neurons -> partial y (f32, or bf16 with ``reduce_dtype=torch.bfloat16``);
+      4. ``scatter``: reduce-scatter the partial y -> y[R_r].
+
+    ``finish`` adds the last layer's y.  NVLink bytes per rank and layer:
+    (N-1)/N T d (2 + 4) (bf16 all-gather + f32 reduce-scatter; 2 + 2 with a bf16 reduce)
+    against (N-1)/N T d 8 for an f32 all-reduce, and the norm and the logits run on T/N
+    rows instead of T.
+
+    The phases are separate methods so a single process can drive N emulated ranks in
+    lockstep (tests); ``layer`` runs them with the real collectives.  ``norm_fn`` /
+    ``ffn_fn`` replace the GPU kernels (CPU tests: the oracle)."""
+
+    def __init__(self, layers, T: int, d: int, rank: int, world: int, device,
+                 comm=None, gain=None, reduce_dtype=torch.float32, dense_first_last=True,
+                 norm_fn=None, ffn_fn=None, x_dtype=torch.bfloat16):
+        if reduce_dtype not in (torch.float32, torch.bfloat16):
+            raise ValidationError("reduce_dtype must be float32 or bfloat16")
+        self.layers = layers  # [(packed shard, DevicePredictor, k)]
+        self.T, self.d, self.rank, self.world = T, d, rank, world
+        self.r0, self.r1 = seq_rows(T, rank, world)
+        dev = torch.device(device)
+        self.dev = dev
+        if comm is None and dist.is_available() and dist.is_initialized():
+            comm = TorchComm()
+        self.comm = comm  # None: a lockstep driver moves the data between the phases
+        self.reduce_dtype = reduce_dtype
+        self.dense_first_last = dense_first_last
+        n = self.r1 - self.r0
+        self.gain = gain if gain is not None else torch.ones(d, device=dev)
+        self.x_shard = torch.empty((n, d), dtype=x_dtype, device=dev)
+        self.lg_shard = torch.empty((n,), dtype=torch.float32, device=dev)
+        self.x_full = torch.empty((T, d), dtype=x_dtype, device=dev)
+        self.lg_full = torch.empty((T,), dtype=torch.float32, device=dev)
+        self.y_part = torch.empty((T, d), dtype=reduce_dtype, device=dev)
+        self.y_shard = torch.empty((n, d), dtype=reduce_dtype, device=dev)
+        self.norm_fn = norm_fn or self._gpu_norm
+        self.ffn_fn = ffn_fn or self._gpu_ffn
+        self.workspace = None
+        self.pending = False  # y_shard holds a layer output not yet added to h
+
+    # -- default (GPU) compute
+    def _gpu_norm(self, l, h_shard, add):
+        from .norm import rmsnorm
+        rmsnorm(h_shard, self.gain, out=self.x_shard, predictor=self.layers[l][1],
+                logits=self.lg_shard, add=add)
+
+    def _gpu_ffn(self, l, x_full, lg_full, y_part):
+        packed, dp, k = self.layers[l]
+        if self.workspace is None:
+            n = max(layer_workspace_bytes(self.T, p, q.r, kk, self.dense_first_last)
+                    for p, q, kk in self.layers)
+            self.workspace = torch.empty(n, dtype=torch.uint8, device=self.dev)
+        if y_part.dtype == torch.float32:
+            sparse_ffn_layer(x_full, packed, dp, k, out=y_part, logits_in=lg_full,
+                             workspace=self.workspace, dense_first_last=self.dense_first_last)
+        else:
+            sparse_ffn_layer(x_full, packed, dp, k, x_next=y_part, f32_out=False,
+                             logits_in=lg_full, workspace=self.workspace,
+                             dense_first_last=self.dense_first_last)
+
+    # -- phases
+    def norm(self, l: int, h_shard: torch.Tensor) -> None:
+        self.norm_fn(l, h_shard, self.y_shard if self.pending else None)
+        self.pending = False
+
+    def gather(self) -> None:
+        self.comm.all_gather(self.x_full, self.x_shard)
+        self.comm.all_gather(self.lg_full, self.lg_shard)
+
+    def ffn(self, l: int) -> None:
+        self.ffn_fn(l, self.x_full, self.lg_full, self.y_part)
+
+    def scatter(self) -> None:
+        self.comm.reduce_scatter(self.y_shard, self.y_part)
+        self.pending = True
+
+    def finish(self, h_shard: torch.Tensor) -> torch.Tensor:
+        if self.pending:
+            h_shard.add_(self.y_shard.to(h_shard.dtype))
+            self.pending = False
+        return h_shard
+
+    def layer(self, l: int, h_shard: torch.Tensor) -> None:
+        self.norm(l, h_shard)
+        self.gather()
+        self.ffn(l)
+        self.scatter()
+
+    def stack(self, h_shard: torch.Tensor) -> torch.Tensor:
+        """Every layer over this rank's residual rows (h_shard f32 [T/N x d], in place)."""
+        for l in range(len(self.layers)):
+            self.layer(l, h_shard)
+        return self.finish(h_shard)

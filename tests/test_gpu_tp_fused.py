@@ -255,12 +255,17 @@ def test_overlapped_layer_across_processes(ff):
     assert _spawn_two(_ipc_overlap_worker) == [(0, True), (1, True)]
 
 
-@pytest.mark.parametrize("collective", ["fused", "overlap"])
-def test_bench_tensor_parallel_fused_path_runs(ff, collective):
-    """bench.py under torchrun, 2 ranks, --collective fused, emulated on the one GPU (gloo
-    for the host-side rendezvous, both ranks time-sliced on GPU 0): the TP sharding, the
-    CUDA IPC peer buffers and the fused completion run end to end and the JSON line is
-    well formed.  (Timings from this emulation are meaningless.)"""
+@pytest.mark.parametrize("collective,extra", [("rs_ag", []), ("rs_ag", ["--reduce-dtype", "bf16"]),
+                                              ("allreduce", ["--skip-alt"]),
+                                              ("fused", ["--skip-alt"]),
+                                              ("overlap", ["--skip-alt"])])
+def test_bench_tensor_parallel_paths_run(ff, collective, extra):
+    """bench.py under torchrun, 2 ranks, emulated on the one GPU (gloo for the collectives,
+    staged through the host where gloo has no CUDA path; both ranks time-sliced on GPU 0):
+    the default N>1 line (TP over d_ffn with the sequence-parallel residual, plus the
+    sequence- and data-parallel splits as extra keys) and the all-reduce / peer-memory
+    completions run end to end and the JSON line is well formed.  (Timings from this
+    emulation are meaningless.)"""
     import json
     import os
     import socket
@@ -274,10 +279,13 @@ def test_bench_tensor_parallel_fused_path_runs(ff, collective):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "2",
            "--config", "1b", "--layers", "2", "--steps", "2", "--warmup", "3",
-           "--parallel", "tp", "--collective", collective]
+           "--parallel", "tp", "--collective", collective] + extra
     r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=400)
     assert r.returncode == 0, r.stderr[-3000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
     d = json.loads(line)
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "tp2"
-    assert d["config"]["collective"] == collective and d["value"] > 0
+    assert d["collective"] and d["value"] > 0
+    if collective == "rs_ag" and not extra:
+        assert set(d["other_splits"]) == {"sp", "dp"}
+        assert all(v["ms_per_layer"] > 0 for v in d["other_splits"].values())

@@ -138,3 +138,117 @@ def test_seq_shard_rules():
     assert dense_first_last_code(1) == 1 and dense_first_last_code(0) == 0
     with pytest.raises(ValidationError):
         dense_first_last_code("middle")
+
+
+def _rms_bf16(h, gain, eps=1e-6):  # kernels.py:96-106, then the bf16 FFN operand
+    h64 = h.astype(np.float64)
+    scale = 1.0 / np.sqrt((h64 * h64).mean(axis=1, keepdims=True) + eps)
+    return orc.bf16_round((h64 * scale * gain.astype(np.float64)).astype(np.float32))
+
+
+def _sp_tp_model(d=512, f=1376, L=2, seed=31):
+    layers = []
+    for l in range(L):
+        lw = orc.random_layer(np.random.default_rng([seed, l]), d, f, 0.02)
+        lw = {k: orc.bf16_round(lw[k]) for k in ("w_gate", "w_up", "w_down")}
+        pred = orc.init_predictor(np.random.default_rng([seed, l, 1]), d, f)
+        comp = {k: orc.bf16_round(v) for k, v in
+                orc.init_compensator(np.random.default_rng([seed, l, 2]), d).items()}
+        layers.append((lw, pred, comp, orc.budget_to_k(0.5, f)))
+    return layers
+
+
+def _ffn_blocks(x, lw, pred, comp, k, nid=None, rank=0, world=1):
+    """The engine's FFN branch over all blocks of x (engine.py:254-310), on the neuron
+    shard `nid` (strided, rank of world) when given; returns (y, global index rows)."""
+    T = x.shape[0]
+    n_blk = T // 128
+    y = np.zeros_like(x)
+    sel = {}
+    gs, us, ds = lw["w_gate"], lw["w_up"], lw["w_down"]
+    c1, c2 = comp["w1"], comp["w2"]
+    if nid is not None:
+        gs, us, ds = gs[:, nid], us[:, nid], ds[nid]
+        from paper_2602_00397_b200.layer import shard_comp_cols
+        lo, hi = shard_comp_cols(c1.shape[1], rank, world)
+        c1, c2 = c1[:, lo:hi], c2[lo:hi]
+    for j in range(n_blk):
+        xb = x[j * 128:(j + 1) * 128]
+        if j in (0, n_blk - 1):
+            y[j * 128:(j + 1) * 128] = orc.dense_ffn(xb, gs, us, ds)
+            continue
+        s = orc.predictor_forward(pred["query"], pred["w1"], pred["w2"], xb)
+        g = orc.topk_indices(s, k)
+        sel[j] = g
+        loc = g if nid is None else g[g % world == rank] // world
+        yb = orc.sparse_ffn_forward(xb, gs, us, ds, loc) if loc.size else 0.0
+        y[j * 128:(j + 1) * 128] = yb + (orc.compensator_forward(c1, c2, xb) if c1.shape[1]
+                                         else 0.0)
+    return y, sel
+
+
+def _sp_tp_worker(rank, world, port, out):
+    """SeqParallelTP with gloo collectives and the oracle in place of the kernels: each
+    rank owns T/N residual rows, normalises them, all-gathers x and the logits, runs the
+    FFN branch on its strided d_ffn shard, reduce-scatters the partial y."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2602_00397_b200.layer import shard_neurons
+        from paper_2602_00397_b200.tp import SeqParallelTP, TorchComm, seq_rows
+        model = _sp_tp_model()
+        d, f, T = 512, 1376, 1024
+        gain = np.ones(d, np.float32)
+        h0 = orc.bf16_round(np.random.default_rng(5).standard_normal((T, d)).astype(np.float32))
+        r0, r1 = seq_rows(T, rank, world)
+        nid = shard_neurons(f, rank, world)
+        log = {"sel_ok": True, "lg_ok": True}
+
+        def norm_fn(l, h_shard, add):
+            if add is not None:
+                h_shard.add_(add)  # engine.py:308 then :267
+            x = _rms_bf16(h_shard.numpy(), gain)
+            sp.x_shard.copy_(torch.from_numpy(x))
+            q = model[l][1]["query"]
+            sp.lg_shard.copy_(torch.from_numpy(orc.mm(q, x.T)[0] / np.float32(np.sqrt(d))))
+
+        def ffn_fn(l, x_full, lg_full, y_part):
+            lw, pred, comp, k = model[l]
+            x = x_full.numpy()
+            want_lg = orc.mm(pred["query"], x.T)[0] / np.float32(np.sqrt(d))
+            log["lg_ok"] &= bool(np.array_equal(lg_full.numpy(), want_lg))
+            y, sel = _ffn_blocks(x, lw, pred, comp, k, nid, rank, world)
+            _, sel_full = _ffn_blocks(x, lw, pred, comp, k)
+            log["sel_ok"] &= all(np.array_equal(sel[j], sel_full[j]) for j in sel)
+            y_part.copy_(torch.from_numpy(y))
+
+        sp = SeqParallelTP([None] * len(model), T, d, rank, world, "cpu", comm=TorchComm(),
+                           norm_fn=norm_fn, ffn_fn=ffn_fn, x_dtype=torch.float32)
+        h = torch.from_numpy(h0[r0:r1].copy())
+        sp.stack(h)
+        parts = [None] * world
+        dist.all_gather_object(parts, (r0, h.numpy(), log))
+        if rank == 0:
+            out["parts"] = parts
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_sp_tp2_reduce_scatter_all_gather_matches_reference():
+    """World 2: the sequence-parallel TP stack (reduce-scatter / all-gather around the
+    FFN branch, engine.py:263-308 split over d_ffn and over the residual rows) equals the
+    unsharded reference chain h <- h + FFN(rmsnorm(h)) over two layers."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_sp_tp_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    parts = sorted(out["parts"], key=lambda p: p[0])
+    assert all(p[2]["sel_ok"] and p[2]["lg_ok"] for p in parts)
+    h_tp = np.concatenate([p[1] for p in parts])
+    d, T = 512, 1024
+    h = orc.bf16_round(np.random.default_rng(5).standard_normal((T, d)).astype(np.float32))
+    for lw, pred, comp, k in _sp_tp_model():
+        y, _ = _ffn_blocks(_rms_bf16(h, np.ones(d, np.float32)), lw, pred, comp, k)
+        h = h + y
+    rel = np.linalg.norm(h_tp - h) / np.linalg.norm(h)
+    assert rel < 1e-5, rel  # f32 partial sums vs one accumulation: rounding only
