@@ -48,6 +48,13 @@
 #ifndef FFWD_K3_W_POLICY
 #define FFWD_K3_W_POLICY 0
 #endif
+// L2 prefetch distance of the gathered W_down rows, in K stages (0 = off; measured slower
+// at 2/4/8: profiles/r2_prefetch_ab.txt): each producer
+// warp prefetches its rows of stage kb + P (tile::gather4 prefetch, one instruction per 4
+// rows x BN columns) while it gathers stage kb.
+#ifndef FFWD_K3_PREFETCH
+#define FFWD_K3_PREFETCH 0
+#endif
 // 1: residual loads / Y and next-X stores bypass L2 residency (.cs streaming)
 #ifndef FFWD_K3_STREAM_EPI
 #define FFWD_K3_STREAM_EPI 0
@@ -78,7 +85,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     down_proj_kernel(const __grid_constant__ CUtensorMap tm_h,
                      const __grid_constant__ CUtensorMap tm_w,
                      const __grid_constant__ CUtensorMap tm_wt,
-                     const __grid_constant__ CUtensorMap tm_hh, GemmArgs a) {
+                     const __grid_constant__ CUtensorMap tm_hh,
+                     const __grid_constant__ CUtensorMap tm_wpf, GemmArgs a) {
   constexpr int kBBytes = BK * BN * 2;
   constexpr int kChunks = BN / 64;            // 64-column (128 B) atoms along N
   constexpr uint32_t kLbo = (BK / 8) * 1024;  // MN-direction atom stride
@@ -136,6 +144,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         // take the 2-D tile path: one 64-row box per column atom, issued by warp 0.
         const int kr = kidx(kb);  // K stage actually loaded (reversed tiles sweep downwards)
         const bool contiguous = m.idx_row < 0 || kr * BK >= m.kpad;
+        if constexpr (FFWD_K3_PREFETCH > 0) {
+          // warm L2 with this warp's rows of stage kb + P (gathered P stages from now)
+          const int kp = kb + FFWD_K3_PREFETCH;
+          const bool pf = kp < nk && m.idx_row >= 0 && kidx(kp) * BK < m.kpad;
+          const int prow = pf ? row_of(kp) : 0;
+#pragma unroll
+          for (int q = 0; q < Q / 4; ++q) {
+            const int p0 = __shfl_sync(0xffffffffu, prow, 4 * q);
+            const int p1 = __shfl_sync(0xffffffffu, prow, 4 * q + 1);
+            const int p2 = __shfl_sync(0xffffffffu, prow, 4 * q + 2);
+            const int p3 = __shfl_sync(0xffffffffu, prow, 4 * q + 3);
+            if (pf && lane == 0) tma_prefetch_gather4(&tm_wpf, tl.n0, p0, p1, p2, p3);
+          }
+        }
         if (lane < Q) rows[lane] = cur;
         __syncwarp();
         if (lane == 0) {
@@ -315,6 +337,9 @@ cudaError_t launch_bn(const GemmArgs& a, cudaStream_t s) {
     return cudaErrorInvalidValue;
   if (encode_tmap_2d_bf16(&twt, a.wd, a.d, a.wd_rows, 64, BK) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
+  CUtensorMap twpf;  // L2 prefetch of whole BN-column row segments
+  if (encode_tmap_2d_bf16_sw(&twpf, a.wd, a.d, a.wd_rows, BN, 1, false) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
   constexpr size_t smem = smem_bytes<BK * BN * 2>();
   static std::atomic<uint64_t> attr{0};
   if (cudaError_t e = ensure_smem_limit(down_proj_kernel<BN>, smem, attr); e != cudaSuccess)
@@ -325,7 +350,7 @@ cudaError_t launch_bn(const GemmArgs& a, cudaStream_t s) {
     if (grid < 2) grid = 2;
   }
   return launch_k(down_proj_kernel<BN>, dim3(grid), dim3(kThreads), smem, s, kPairA ? 2 : 1, th,
-                  tw, twt, thh, a);
+                  tw, twt, thh, twpf, a);
 }
 
 }  // namespace

@@ -147,5 +147,7 @@ cudaError_t launch_down_proj(const GemmArgs& a, cudaStream_t s);
 // tensor-map encoder (driver entry point resolved once through the runtime)
 CUresult encode_tmap_2d_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows,
                              uint32_t box_inner, uint32_t box_rows);
+CUresult encode_tmap_2d_bf16_sw(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows,
+                                uint32_t box_inner, uint32_t box_rows, bool swizzle128);
 
 }  // namespace ffwd

@@ -25,6 +25,7 @@
 #include "ffwd_internal.h"
 #include "launch.cuh"
 #include "rowdot.cuh"
+#include "widen.cuh"
 
 namespace ffwd {
 
@@ -104,9 +105,26 @@ __global__ void __launch_bounds__(kNormThreads, 2)
     if (row + static_cast<int>(gridDim.x) < T) load_row(row + gridDim.x, nxt);  // prefetch
     double xd[kMaxV][4];
     double ss = 0.0;
+    bool special = false;  // widen on the INT pipe unless a lane holds 0/subnormal/inf/NaN
 #pragma unroll
     for (int j = 0; j < kMaxV; ++j) {
-      xd[j][0] = v[j].x; xd[j][1] = v[j].y; xd[j][2] = v[j].z; xd[j][3] = v[j].w;
+      if (threadIdx.x + kNormThreads * j < nv)
+        special |= widen::f32_special(__float_as_uint(v[j].x)) ||
+                   widen::f32_special(__float_as_uint(v[j].y)) ||
+                   widen::f32_special(__float_as_uint(v[j].z)) ||
+                   widen::f32_special(__float_as_uint(v[j].w));
+    }
+    const bool fast = !__any_sync(0xffffffffu, special);
+#pragma unroll
+    for (int j = 0; j < kMaxV; ++j) {
+      if (fast) {
+        xd[j][0] = widen::f32_normal_to_f64(__float_as_uint(v[j].x));
+        xd[j][1] = widen::f32_normal_to_f64(__float_as_uint(v[j].y));
+        xd[j][2] = widen::f32_normal_to_f64(__float_as_uint(v[j].z));
+        xd[j][3] = widen::f32_normal_to_f64(__float_as_uint(v[j].w));
+      } else {
+        xd[j][0] = v[j].x; xd[j][1] = v[j].y; xd[j][2] = v[j].z; xd[j][3] = v[j].w;
+      }
       ss += (xd[j][0] * xd[j][0] + xd[j][1] * xd[j][1]) +
             (xd[j][2] * xd[j][2] + xd[j][3] * xd[j][3]);
     }
@@ -136,9 +154,20 @@ __global__ void __launch_bounds__(kNormThreads, 2)
         if constexpr (kLogitF32) {
           rowdot::accumulate(z, qd[j], o);
         } else {
-          const float2 l2 = __bfloat1622float2(lo), h2 = __bfloat1622float2(hi);
-          const float xb[4] = {l2.x, l2.y, h2.x, h2.y};
-          rowdot::accumulate(z, qd[j], xb);
+          const uint32_t wl = *reinterpret_cast<const uint32_t*>(&lo);
+          const uint32_t wh = *reinterpret_cast<const uint32_t*>(&hi);
+          if (!__any_sync(__activemask(),
+                          widen::bf16x2_special(wl) || widen::bf16x2_special(wh))) {
+            // exact bf16 -> f64 on the INT pipe (same values as the F2F path below)
+            z[0] = fma(qd[j][0], widen::bf16_normal_to_f64(wl), z[0]);
+            z[1] = fma(qd[j][1], widen::bf16_normal_to_f64(wl >> 16), z[1]);
+            z[2] = fma(qd[j][2], widen::bf16_normal_to_f64(wh), z[2]);
+            z[3] = fma(qd[j][3], widen::bf16_normal_to_f64(wh >> 16), z[3]);
+          } else {
+            const float2 l2 = __bfloat1622float2(lo), h2 = __bfloat1622float2(hi);
+            const float xb[4] = {l2.x, l2.y, h2.x, h2.y};
+            rowdot::accumulate(z, qd[j], xb);
+          }
         }
       }
     }

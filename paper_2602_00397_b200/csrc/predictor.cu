@@ -34,6 +34,7 @@
 #define FFWD_POOL_MINB 3
 #endif
 #include "rowdot.cuh"
+#include "widen.cuh"
 #include "sm100.cuh"
 
 namespace ffwd {
@@ -228,11 +229,31 @@ __global__ void __launch_bounds__(kPoolThreads, FFWD_POOL_MINB)
         if (t0 + u < n) xr[u].load(x, static_cast<size_t>(tok0 + t0 + u) * d + c);
         else xr[u].zero();
       }
+      bool special = false;  // bf16: widen on the INT pipe unless a lane holds 0/subnormal/inf/NaN
+      if constexpr (!kF32) {
 #pragma unroll
-      for (int u = 0; u < kBatch; ++u) {
-        const double pt = probd[t0 + u];
+        for (int u = 0; u < kBatch; ++u) {
+          const uint32_t* w = reinterpret_cast<const uint32_t*>(xr[u].v);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = fma(pt, xr[u].get(i), acc[i]);
+          for (int q = 0; q < 4; ++q) special |= widen::bf16x2_special(w[q]);
+        }
+      }
+      if (kF32 || __any_sync(__activemask(), special)) {
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const double pt = probd[t0 + u];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = fma(pt, xr[u].get(i), acc[i]);
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+          const double pt = probd[t0 + u];
+          const uint32_t* w = reinterpret_cast<const uint32_t*>(xr[u].v);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            acc[i] = fma(pt, widen::bf16_normal_to_f64(w[i >> 1] >> (16 * (i & 1))), acc[i]);
+        }
       }
     }
   }

@@ -109,6 +109,17 @@ __device__ __forceinline__ void tma_gather4(const CUtensorMap* m, uint64_t* bar,
       : "memory");
 }
 
+// L2 prefetch of four arbitrary rows (tile::gather4 addressing, no shared-memory
+// destination, no barrier): warms L2 with a later stage's gathered rows.
+__device__ __forceinline__ void tma_prefetch_gather4(const CUtensorMap* m, int32_t c0, int32_t r0,
+                                                     int32_t r1, int32_t r2, int32_t r3) {
+  asm volatile(
+      "cp.async.bulk.prefetch.tensor.2d.L2.global.tile::gather4 [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
+
 // 2-D tile load multicast to the CTAs in `mask` of this cluster: the box lands at the
 // same shared-memory offset in every destination CTA and completes tx on the mbarrier
 // at `bar`'s offset there.

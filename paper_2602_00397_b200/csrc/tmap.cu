@@ -32,10 +32,19 @@ EncodeFn get_encode() {
 
 }  // namespace
 
+CUresult encode_tmap_2d_bf16_sw(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows,
+                                uint32_t box_inner, uint32_t box_rows, bool swizzle128);
+
 // 2-D bf16 row-major tensor [rows x inner], 128 B swizzle, box {box_inner, box_rows};
 // out-of-bounds rows of a box read as zero (the short tail block).
 CUresult encode_tmap_2d_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows,
                              uint32_t box_inner, uint32_t box_rows) {
+  return encode_tmap_2d_bf16_sw(m, base, inner, rows, box_inner, box_rows, true);
+}
+
+// swizzle128 = false: no swizzle (boxes wider than 128 B; L2 prefetch maps)
+CUresult encode_tmap_2d_bf16_sw(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows,
+                                uint32_t box_inner, uint32_t box_rows, bool swizzle128) {
   EncodeFn enc = get_encode();
   if (!enc) return CUDA_ERROR_NOT_FOUND;
   const cuuint64_t dims[2] = {inner, rows};
@@ -43,7 +52,8 @@ CUresult encode_tmap_2d_bf16(CUtensorMap* m, const void* base, uint64_t inner, u
   const cuuint32_t box[2] = {box_inner, box_rows};
   const cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
-             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 

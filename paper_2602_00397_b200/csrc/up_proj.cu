@@ -35,6 +35,14 @@
 #include "gemm_sm100.cuh"
 #include "launch.cuh"
 
+// L2 prefetch distance of the gathered gate/up rows, in K stages (0 = off, measured slower
+// at 4/8/16: profiles/r2_prefetch_ab.txt; a multiple of
+// 4): every 4 stages each producer warp prefetches its rows' next 4 column chunks
+// (256 columns, tile::gather4 prefetch) P stages ahead of the gathers.
+#ifndef FFWD_K2_PREFETCH
+#define FFWD_K2_PREFETCH 0
+#endif
+
 namespace ffwd {
 
 namespace {
@@ -48,7 +56,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     up_proj_kernel(const __grid_constant__ CUtensorMap tm_x,
                    const __grid_constant__ CUtensorMap tm_w,
                    const __grid_constant__ CUtensorMap tm_wt,
-                   const __grid_constant__ CUtensorMap tm_xh, GemmArgs a) {
+                   const __grid_constant__ CUtensorMap tm_xh,
+                   const __grid_constant__ CUtensorMap tm_wpf, GemmArgs a) {
   extern __shared__ uint8_t smem_raw[];
   Smem<kBBytes> sm(smem_raw);
   const int warp = threadIdx.x >> 5;
@@ -111,6 +120,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_load_2d(&tm_wt, &sm.bar->full[stage], sm.b_stage(stage), kb * BK, r0, pol_w);
               tma_load_2d(&tm_wt, &sm.bar->full[stage], sm.b_stage(stage) + 128 * 128, kb * BK,
                           r1, pol_w);
+            }
+          }
+          if constexpr (FFWD_K2_PREFETCH > 0) {
+            const int kp = kb + FFWD_K2_PREFETCH;
+            if (!contiguous && (kb & 3) == 0 && kp < nk) {
+#pragma unroll
+              for (int q = 0; q < R / 4; ++q) {
+                const int4 r = rq[q];
+                tma_prefetch_gather4(&tm_wpf, kp * BK, r.x, r.y, r.z, r.w);
+              }
             }
           }
           if (!contiguous) {
@@ -259,6 +278,9 @@ cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s) {
     return cudaErrorInvalidValue;
   if (encode_tmap_2d_bf16(&twt, a.wgu_t, a.d, a.wgu_rows, BK, 128) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
+  CUtensorMap twpf;  // L2 prefetch: 4 column chunks of 4 gathered rows per instruction
+  if (encode_tmap_2d_bf16_sw(&twpf, a.wgu_t, a.d, a.wgu_rows, 4 * BK, 1, false) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
   constexpr size_t smem = smem_bytes<kBBytes>();
   static std::atomic<uint64_t> attr{0};
   if (cudaError_t e = ensure_smem_limit(up_proj_kernel, smem, attr); e != cudaSuccess) return e;
@@ -268,7 +290,7 @@ cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s) {
     if (grid < 2) grid = 2;
   }
   return launch_k(up_proj_kernel, dim3(grid), dim3(kThreads), smem, s, kPairA ? 2 : 1, tx, tw, twt,
-                  txh, a);
+                  txh, twpf, a);
 }
 
 }  // namespace ffwd
