@@ -77,10 +77,13 @@ def test_dense_first_last_codes(ff):
         ff.sparse_ffn_layer(x, packed, dp, k, dense_first_last="middle")
 
 
-def test_bench_sequence_parallel_runs(ff):
-    """bench.py under torchrun, 2 ranks, default --parallel sp, emulated on the one GPU
-    (gloo rendezvous, both ranks time-sliced on GPU 0): each rank runs its half of the
-    prompt's blocks with no collective; the JSON line is well formed."""
+@pytest.mark.parametrize("parallel", [None, "sp", "dp"])
+def test_bench_multi_rank_runs(ff, parallel):
+    """bench.py under torchrun, 2 ranks, emulated on the one GPU (gloo rendezvous, both
+    ranks time-sliced on GPU 0). Default (None) = tensor parallel over d_ffn (the north
+    star's split) with the sequence-parallel residual; sp = the prompt's blocks split with
+    no collective; dp = one prompt per rank (BASELINE configs[4], weak scaling). The JSON
+    line must be well formed and name the split."""
     import json
     import os
     import socket
@@ -94,9 +97,13 @@ def test_bench_sequence_parallel_runs(ff):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "2",
            "--config", "1b", "--layers", "2", "--steps", "2", "--warmup", "3"]
+    if parallel is not None:
+        cmd += ["--parallel", parallel]
     r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=400)
     assert r.returncode == 0, r.stderr[-3000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
     d = json.loads(line)
-    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "sp2"
-    assert d["scaling"] == "strong" and d["value"] > 0 and d["e2e"]["value"] > 0
+    want = {None: "tp2", "sp": "sp2", "dp": "dp2"}[parallel]
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == want
+    assert d["scaling"] == ("weak" if parallel == "dp" else "strong")
+    assert d["value"] > 0 and d["e2e"]["value"] > 0
