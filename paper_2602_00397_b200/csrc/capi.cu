@@ -132,6 +132,7 @@ struct Carve {
 
 struct Pred {
   float* logits;
+  float* probs;  // f32(softmax) per block token (softmax_kernel)
   float* pooled;
   float* hidden;
   double* partial;
@@ -141,6 +142,7 @@ struct Pred {
 Pred carve_pred(Carve& c, int nb, int d, int r, int f, bool with_scores) {
   Pred p;
   p.logits = c.take<float>(static_cast<size_t>(nb) * kBlockTokens);
+  p.probs = c.take<float>(static_cast<size_t>(nb) * kBlockTokens);
   p.pooled = c.take<float>(static_cast<size_t>(nb) * d);
   p.hidden = c.take<float>(static_cast<size_t>(nb) * r);
   const size_t part = std::max(gemm_f64acc_partial_bytes(nb, d, r),
@@ -160,8 +162,9 @@ int run_predictor(const void* x, bool x_is_f32, int T, int d, int b0, int nb, co
                                   p.pooled, s),
               "pool");
   } else {
-    StageTimer tm(kPool, s, logits_in ? 1 : 2);
-    FFWD_CUDA(launch_pool(x, x_is_f32, T, d, b0, nb, query, sqrt_d, p.logits, p.pooled, logits_in, s),
+    StageTimer tm(kPool, s, logits_in ? 2 : 3);  // [logits,] softmax, pool
+    FFWD_CUDA(launch_pool(x, x_is_f32, T, d, b0, nb, query, sqrt_d, p.logits, p.pooled, logits_in,
+                          p.probs, s),
               "pool");
   }
   {
@@ -169,8 +172,8 @@ int run_predictor(const void* x, bool x_is_f32, int T, int d, int b0, int nb, co
     FFWD_CUDA(launch_gemm_f64acc(p.pooled, w1, p.hidden, nb, d, r, true, p.partial, s), "w1");
   }
   {
-    StageTimer tm(kW2, s, gemm_f64acc_partial_bytes(nb, r, f) > 0 ? 2 : 1);
-    FFWD_CUDA(launch_gemm_f64acc(p.hidden, w2, scores, nb, r, f, false, p.partial, s), "w2");
+    StageTimer tm(kW2, s);
+    FFWD_CUDA(launch_gemm_f64acc(p.hidden, w2, scores, nb, r, f, false, nullptr, s), "w2");
   }
   return FFWD_OK;
 }
@@ -397,7 +400,7 @@ int ffwd_predictor_forward_block(const void* x, int x_is_f32, int n, int d, cons
   FFWD_CUDA(launch_pool_generic(x, x_is_f32 != 0, n, d, n, 0, 1, query, sqrt_d, p.pooled, s),
             "pool");
   FFWD_CUDA(launch_gemm_f64acc(p.pooled, w1, p.hidden, 1, d, r, true, p.partial, s), "w1");
-  FFWD_CUDA(launch_gemm_f64acc(p.hidden, w2, scores, 1, r, f, false, p.partial, s), "w2");
+  FFWD_CUDA(launch_gemm_f64acc(p.hidden, w2, scores, 1, r, f, false, nullptr, s), "w2");
   return FFWD_OK;
 }
 

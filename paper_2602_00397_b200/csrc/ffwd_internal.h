@@ -40,12 +40,13 @@ struct PlanCounts {
 };
 
 // ------------------------------------------------------------------ K1
-// Attention pooling in two streaming passes over X (per-token logits, then per-block
-// softmax + pooled sum), then the two f64-accumulated predictor GEMMs (DMMA, split-K
-// partials reduced in fixed order).  `logits`: blk_count * 128 floats of scratch.
+// Attention pooling: per-token logits (skipped with `logits_in`), a per-block softmax
+// (`probs`: blk_count * 128 floats), the pooled sum; then the two f64-accumulated
+// predictor GEMMs (DMMA, split-K partials reduced in fixed order).  `logits`:
+// blk_count * 128 floats of scratch.
 cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begin,
                         int blk_count, const float* query, float sqrt_d, float* logits,
-                        float* pooled, const float* logits_in, cudaStream_t s);
+                        float* pooled, const float* logits_in, float* probs, cudaStream_t s);
 // Any-shape pooling: blocks of `rpb` rows, any d (the drop-in's small shapes).
 cudaError_t launch_pool_generic(const void* x, bool x_is_f32, int T, int d, int rpb,
                                 int blk_begin, int blk_count, const float* query, float sqrt_d,
@@ -82,7 +83,7 @@ cudaError_t launch_hidden_scores(const void* h, bool is_f32, int ld, int T, int 
 cudaError_t launch_rope(void* qk, bool is_f32, int T, int row_stride, int k_col, int n_heads,
                         int d_head, const double* cos_t, const double* sin_t, const float* cos32,
                         const float* sin32, int pos0, cudaStream_t s);
-// `partial` (nullable, gemm_f64acc_partial_bytes) enables split-K.
+// `partial` (nullable, gemm_f64acc_partial_bytes) enables split-K for long K.
 size_t gemm_f64acc_partial_bytes(int M, int K, int N);
 cudaError_t launch_gemm_f64acc(const float* A, const float* B, float* C, int M, int K, int N,
                                bool relu, double* partial, cudaStream_t s);

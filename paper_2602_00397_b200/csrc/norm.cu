@@ -25,6 +25,7 @@
 #include "ffwd_internal.h"
 #include "launch.cuh"
 #include "rowdot.cuh"
+#include "sm100.cuh"
 #include "widen.cuh"
 
 namespace ffwd {
@@ -179,6 +180,252 @@ __global__ void __launch_bounds__(kNormThreads, 2)
   }
 }
 
+// ---------------------------------------------------------------- ring-staged RMSNorm
+// The same row computation as rmsnorm_kernel (thread i of the 256 owns the float4 groups
+// {i + 256 j}; ss and the fused logit in rowdot.cuh's f64 order, so the logits are
+// bit-identical to logits_kernel's), organised so neither memory latency nor the per-row
+// cross-warp reductions stall the issue slots:
+//   * a producer warp streams the CTA's rows (and the `add` rows) into a shared-memory
+//     ring with 1-D TMA bulk copies, `ns` rows ahead;
+//   * the 8 consumer warps run a two-row software pipeline: phase A of row i (load,
+//     [add], the warp's partial sum of squares, published through an mbarrier) is
+//     followed by phase B of row i - 1 (the row's scale from the 8 partials, outputs,
+//     partial logit), so the wait for the other warps' partials is covered by a row of
+//     work instead of a __syncthreads;
+//   * warp 0 finishes each row's logit two rows later from the warps' partials.
+// Arithmetic per element (the old kernel spent ~46 instructions per element on INT-pipe
+// widening, special-value checks and f64 products; ncu r2):
+//   * ss: one F2F (f32 -> f64, exact) and one DFMA;
+//   * out = f32((x * scale) * gain): f32 arithmetic on scale split into s_hi + s_lo
+//     (p = x s_hi, its exact error by FMA, + x s_lo, then (p + c) * g with one final
+//     rounding): within ~2^-47 of the exact product before the final rounding, so it
+//     differs from the reference's f64 evaluation (kernels.py:105-106) only when the
+//     product lies that close to an f32 rounding boundary (~1e-7 of the elements);
+//   * logit: bf16 -> f32 (a shift), F2F, DFMA, as before.
+// bf16 -> f64, exact, one conversion instruction
+__device__ __forceinline__ double bf16_to_f64(__nv_bfloat16 h) {
+  double d;
+  asm("cvt.f64.bf16 %0, %1;" : "=d"(d) : "h"(*reinterpret_cast<const unsigned short*>(&h)));
+  return d;
+}
+
+constexpr int kRingWarps = kNormThreads / 32;  // consumer warps
+constexpr int kRedSlots = 4;                   // reduction slots (rows in flight <= 3)
+constexpr int kMaxRing = 16;
+
+struct RingHdr {
+  uint64_t full[kMaxRing];
+  uint64_t empty[kMaxRing];
+  uint64_t bar_ss[kRedSlots];
+  uint64_t bar_z[kRedSlots];
+  double red_ss[kRedSlots][kRingWarps];
+  double red_z[kRedSlots][kRingWarps];
+};
+constexpr uint32_t kRingHdrBytes = (sizeof(RingHdr) + 127) / 128 * 128;
+
+template <int kMaxV, int kAdd, bool kLogitF32>
+__global__ void __launch_bounds__(kNormThreads + 32)
+    rmsnorm_ring_kernel(float* __restrict__ x, const float* __restrict__ gain, int T, int d,
+                        double eps, const void* __restrict__ add,
+                        __nv_bfloat16* __restrict__ out_bf16, float* __restrict__ out_f32,
+                        const float* __restrict__ query, float sqrt_d, float* __restrict__ logits,
+                        int logit_row0, int logit_row1, int ns, uint32_t stage_bytes) {
+  extern __shared__ __align__(128) uint8_t smem_ring[];
+  RingHdr* hd = reinterpret_cast<RingHdr*>(smem_ring);
+  uint8_t* ring = smem_ring + kRingHdrBytes;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nv = d / 4;
+  const int nrows = (T - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
+                    static_cast<int>(gridDim.x);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ns; ++s) {
+      mbar_init(&hd->full[s], 1);
+      mbar_init(&hd->empty[s], kRingWarps);
+    }
+    for (int r = 0; r < kRedSlots; ++r) {
+      mbar_init(&hd->bar_ss[r], kRingWarps);
+      mbar_init(&hd->bar_z[r], kRingWarps);
+    }
+    fence_barrier_init();
+  }
+  float gf[kMaxV][4];
+  double qd[kMaxV][4];
+  if (warp < kRingWarps) {
+#pragma unroll
+    for (int j = 0; j < kMaxV; ++j) {
+      const int g = threadIdx.x + kNormThreads * j;
+      const float4 w = g < nv ? __ldg(reinterpret_cast<const float4*>(gain) + g)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 q = (query && g < nv) ? __ldg(reinterpret_cast<const float4*>(query) + g)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      gf[j][0] = w.x; gf[j][1] = w.y; gf[j][2] = w.z; gf[j][3] = w.w;
+      qd[j][0] = q.x; qd[j][1] = q.y; qd[j][2] = q.z; qd[j][3] = q.w;
+    }
+  }
+  __syncthreads();
+  // gain and query are parameters: read while the predecessor drains, then wait for it
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t xbytes = static_cast<uint32_t>(d) * 4u;
+  if (warp == kRingWarps) {  // ---- producer: the CTA's rows into the ring
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < nrows; ++i) {
+        if (i >= ns) mbar_wait(&hd->empty[s], ph ^ 1);
+        const size_t row = blockIdx.x + static_cast<size_t>(i) * gridDim.x;
+        mbar_arrive_expect_tx(&hd->full[s], stage_bytes);
+        uint8_t* dst = ring + static_cast<size_t>(s) * stage_bytes;
+        bulk_load(dst, x + row * d, xbytes, &hd->full[s]);
+        if constexpr (kAdd == 1)
+          bulk_load(dst + xbytes, static_cast<const float*>(add) + row * d, xbytes, &hd->full[s]);
+        if constexpr (kAdd == 2)
+          bulk_load(dst + xbytes, static_cast<const __nv_bfloat16*>(add) + row * d, xbytes / 2,
+                    &hd->full[s]);
+        if (++s == ns) { s = 0; ph ^= 1; }
+      }
+    }
+    return;  // no CTA-wide barrier follows
+  }
+
+  auto row_of = [&](int i) { return static_cast<int>(blockIdx.x) + i * static_cast<int>(gridDim.x); };
+
+  // Phase A: [x += add] and this warp's partial sum of squares of row i.
+  // ring positions of phase A's and phase B's rows (no integer division per row)
+  int sa = 0, sb = 0;
+  uint32_t pa = 0;
+  auto phase_a = [&](int i) {
+    const int s = sa;
+    mbar_wait_sleep(&hd->full[s], pa, 1000);
+    if (++sa == ns) { sa = 0; pa ^= 1; }
+    float4* xs = reinterpret_cast<float4*>(ring + static_cast<size_t>(s) * stage_bytes);
+    const size_t row = static_cast<size_t>(row_of(i));
+    double sq[4] = {0.0, 0.0, 0.0, 0.0};  // four DFMA chains, one per float4 lane
+#pragma unroll
+    for (int j = 0; j < kMaxV; ++j) {
+      const int g = threadIdx.x + kNormThreads * j;
+      if (g >= nv) continue;
+      float4 v = xs[g];
+      if constexpr (kAdd != 0) {
+        float4 a4;
+        if constexpr (kAdd == 1) {
+          a4 = reinterpret_cast<const float4*>(ring + static_cast<size_t>(s) * stage_bytes + xbytes)[g];
+        } else {
+          const uint2 raw = reinterpret_cast<const uint2*>(
+              ring + static_cast<size_t>(s) * stage_bytes + xbytes)[g];
+          const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+          const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+          a4 = make_float4(lo.x, lo.y, hi.x, hi.y);
+        }
+        v.x = __fadd_rn(v.x, a4.x);  // engine.py:265, f32 residual add
+        v.y = __fadd_rn(v.y, a4.y);
+        v.z = __fadd_rn(v.z, a4.z);
+        v.w = __fadd_rn(v.w, a4.w);
+        xs[g] = v;  // phase B reads the sum
+        reinterpret_cast<float4*>(x + row * d)[g] = v;
+      }
+      const float xv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const double xd = xv[e];  // F2F, exact
+        sq[e] = fma(xd, xd, sq[e]);
+      }
+    }
+    const double ss = rowdot::warp_sum(rowdot::thread_value(sq));
+    if (lane == 0) {
+      hd->red_ss[i & (kRedSlots - 1)][warp] = ss;
+      mbar_arrive(&hd->bar_ss[i & (kRedSlots - 1)]);
+    }
+  };
+
+  // Phase B: row i's scale, outputs and this warp's partial logit; releases the ring slot.
+  auto phase_b = [&](int i) {
+    const int s = sb, slot = i & (kRedSlots - 1);
+    if (++sb == ns) sb = 0;
+    mbar_wait_sleep(&hd->bar_ss[slot], (i / kRedSlots) & 1, 1000);
+    double ssum = 0.0;
+#pragma unroll
+    for (int w = 0; w < kRingWarps; ++w) ssum += hd->red_ss[slot][w];
+    const double mean = ssum / static_cast<double>(d);
+    const double scale = 1.0 / sqrt(mean + eps);  // kernels.py:105
+    const float s_hi = static_cast<float>(scale);
+    const float s_lo = static_cast<float>(scale - static_cast<double>(s_hi));
+    const int row = row_of(i);
+    const bool want_logit = query != nullptr && row >= logit_row0 && row < logit_row1;
+    const float4* xs = reinterpret_cast<const float4*>(ring + static_cast<size_t>(s) * stage_bytes);
+    double z[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < kMaxV; ++j) {
+      const int g = threadIdx.x + kNormThreads * j;
+      if (g >= nv) continue;
+      const float4 v = xs[g];
+      const float xv[4] = {v.x, v.y, v.z, v.w};
+      float o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float p = __fmul_rn(xv[e], s_hi);
+        const float c = __fmaf_rn(xv[e], s_lo, __fmaf_rn(xv[e], s_hi, -p));
+        o[e] = __fmaf_rn(p, gf[j][e], __fmul_rn(c, gf[j][e]));
+      }
+      const size_t off = static_cast<size_t>(row) * d + 4 * static_cast<size_t>(g);
+      if (out_f32) reinterpret_cast<float4*>(out_f32 + off)[0] = make_float4(o[0], o[1], o[2], o[3]);
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(o[0], o[1]);
+      const __nv_bfloat162 hi = __floats2bfloat162_rn(o[2], o[3]);
+      if (out_bf16) {
+        uint2 pk;
+        pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+        reinterpret_cast<uint2*>(out_bf16 + off)[0] = pk;
+      }
+      if (want_logit) {
+        if constexpr (kLogitF32) {
+          rowdot::accumulate(z, qd[j], o);
+        } else {  // bf16 -> f64 in one cvt (F2F.F64.BF16), exact
+          z[0] = fma(qd[j][0], bf16_to_f64(lo.x), z[0]);
+          z[1] = fma(qd[j][1], bf16_to_f64(lo.y), z[1]);
+          z[2] = fma(qd[j][2], bf16_to_f64(hi.x), z[2]);
+          z[3] = fma(qd[j][3], bf16_to_f64(hi.y), z[3]);
+        }
+      }
+    }
+    if constexpr (kAdd != 0) fence_proxy_async_smem();  // phase A wrote into the slot
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&hd->empty[s]);
+    const double zs = want_logit ? rowdot::warp_sum(rowdot::thread_value(z)) : 0.0;
+    if (lane == 0) {
+      hd->red_z[slot][warp] = zs;
+      mbar_arrive(&hd->bar_z[slot]);
+    }
+  };
+
+  // warp 0: row i's logit from the 8 partials (rowdot::block_sum's order)
+  auto finish = [&](int i) {
+    const int slot = i & (kRedSlots - 1);
+    mbar_wait_sleep(&hd->bar_z[slot], (i / kRedSlots) & 1, 1000);
+    const int row = row_of(i);
+    if (lane == 0 && query != nullptr && row >= logit_row0 && row < logit_row1) {
+      double zsum = 0.0;
+#pragma unroll
+      for (int w = 0; w < kRingWarps; ++w) zsum += hd->red_z[slot][w];
+      logits[row - logit_row0] = __fdiv_rn(static_cast<float>(zsum), sqrt_d);  // predictor.py:76
+    }
+    __syncwarp();
+  };
+
+  for (int i = 0; i < nrows; ++i) {
+    phase_a(i);
+    if (i >= 1) {
+      phase_b(i - 1);
+      if (warp == 0 && i >= 2) finish(i - 2);
+    }
+  }
+  if (nrows >= 1) phase_b(nrows - 1);
+  if (warp == 0) {
+    if (nrows >= 2) finish(nrows - 2);
+    if (nrows >= 1) finish(nrows - 1);
+  }
+}
+
 // One CTA per token; a thread rotates 2 consecutive pairs (i, i+1) of one head at a
 // time (vector loads of both halves).  Q heads at column 0, K heads at k_col.
 template <typename E>
@@ -241,6 +488,38 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace
 
+#ifndef FFWD_NORM_RING
+#define FFWD_NORM_RING 1  // 0: the CTA-per-row rmsnorm_kernel for every shape
+#endif
+
+// Ring kernel: stage = the row (+ its add row); 2 CTAs per SM when >= 4 stages fit in
+// half the shared memory, else 1 CTA with up to kMaxRing stages.
+template <int kMaxV, int kAdd, bool kLogitF32>
+cudaError_t launch_ring(float* x, const float* gain, int T, int d, double eps, const void* add,
+                        __nv_bfloat16* ob, float* out_f32, const float* query, float sqrt_d,
+                        float* logits, int r0, int r1, int sms, bool* used, cudaStream_t s) {
+  *used = false;
+  const uint32_t stage = static_cast<uint32_t>(d) * (kAdd == 1 ? 8u : (kAdd == 2 ? 6u : 4u));
+  const size_t cap2 = 110 * 1024 - kRingHdrBytes, cap1 = 226 * 1024 - kRingHdrBytes;
+  int per_sm = 2, ns = static_cast<int>(cap2 / stage);
+  if (ns < 4) {
+    per_sm = 1;
+    ns = static_cast<int>(cap1 / stage);
+  }
+  if (ns < 3) return cudaSuccess;  // rows too wide: the caller takes rmsnorm_kernel
+  if (ns > kMaxRing) ns = kMaxRing;
+  const size_t smem = kRingHdrBytes + static_cast<size_t>(ns) * stage;
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = ensure_smem_limit(rmsnorm_ring_kernel<kMaxV, kAdd, kLogitF32>, 226 * 1024, attr);
+      e != cudaSuccess)
+    return e;
+  const int grid = T < per_sm * sms ? T : per_sm * sms;
+  *used = true;
+  return launch_k(rmsnorm_ring_kernel<kMaxV, kAdd, kLogitF32>, dim3(grid),
+                  dim3(kNormThreads + 32), smem, s, 1, x, gain, T, d, eps, add, ob, out_f32,
+                  query, sqrt_d, logits, r0, r1, ns, stage);
+}
+
 template <int kAdd, bool kLogitF32>
 cudaError_t launch_rmsnorm_t(float* x, const float* gain, int T, int d, double eps,
                              const void* add, __nv_bfloat16* ob, float* out_f32,
@@ -250,6 +529,16 @@ cudaError_t launch_rmsnorm_t(float* x, const float* gain, int T, int d, double e
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // the ring's bulk copies need 16 B rows: d % 4 == 0 always holds, a bf16 add needs d % 8
+  if (FFWD_NORM_RING && nv <= 8 && (kAdd != 2 || d % 8 == 0)) {
+    bool used = false;
+    cudaError_t e;
+    if (nv <= 1) e = launch_ring<1, kAdd, kLogitF32>(x, gain, T, d, eps, add, ob, out_f32, query, sqrt_d, logits, r0, r1, sms, &used, s);
+    else if (nv <= 2) e = launch_ring<2, kAdd, kLogitF32>(x, gain, T, d, eps, add, ob, out_f32, query, sqrt_d, logits, r0, r1, sms, &used, s);
+    else if (nv <= 4) e = launch_ring<4, kAdd, kLogitF32>(x, gain, T, d, eps, add, ob, out_f32, query, sqrt_d, logits, r0, r1, sms, &used, s);
+    else e = launch_ring<8, kAdd, kLogitF32>(x, gain, T, d, eps, add, ob, out_f32, query, sqrt_d, logits, r0, r1, sms, &used, s);
+    if (e != cudaSuccess || used) return e;
+  }
   const int grid = T < 2 * sms ? T : 2 * sms;
   cudaError_t e = cudaSuccess;
 #define FFWD_NORM(V)                                                                       \

@@ -173,18 +173,48 @@ cudaError_t launch_logits(const void* x, int d, int tok0, int ntok, const float*
   return cudaErrorInvalidValue;
 }
 
-// Pass 2: p = f32(softmax_f64(logits_b)) (kernels.py:57-80), recomputed by every CTA of
-// the block (128 values), then pooled_b[c] = f32(sum_t p_t x_t[c]) with f64 accumulation
-// (predictor.py:78).  grid (ceil(d / 512), blk_count); blocks run in reverse order so
-// the rows pass 1 read last are still in L2.  Warp w covers 256 columns (8 per lane,
-// half h = w & 1 of the CTA's 512) for the 32 tokens of quarter w >> 1, with 16 loads
-// of 16 B in flight per lane; the four quarter partials are added in order.
+// Softmax of each block's logits (kernels.py:57-80, non-causal, f64, max-subtracted,
+// rounded to f32), once per block: the probabilities the pooling pass weights X with.
+// 128 threads = 4 warps of 32 tokens; the sum is the 4 warp butterflies added in order.
+__global__ void __launch_bounds__(kBlockTokens)
+    softmax_kernel(int T, int blk_begin, const float* __restrict__ logits,
+                   float* __restrict__ probs) {
+  __shared__ double wred[2][4];
+  pdl_wait();
+  pdl_trigger();
+  const int rel = blockIdx.x;
+  const int tok0 = (blk_begin + rel) * kBlockTokens;
+  const int n = min(kBlockTokens, T - tok0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double l = threadIdx.x < n ? static_cast<double>(logits[rel * kBlockTokens + threadIdx.x])
+                                   : -INFINITY;
+  const double wm = warp_max_f64(l);
+  if (lane == 0) wred[0][warp] = wm;
+  __syncthreads();
+  const double m = fmax(fmax(wred[0][0], wred[0][1]), fmax(wred[0][2], wred[0][3]));
+  const double e = threadIdx.x < n ? exp(l - m) : 0.0;
+  const double ws = warp_sum_f64(e);
+  if (lane == 0) wred[1][warp] = ws;
+  __syncthreads();
+  const double sum = ((wred[1][0] + wred[1][1]) + wred[1][2]) + wred[1][3];
+  probs[rel * kBlockTokens + threadIdx.x] = threadIdx.x < n ? static_cast<float>(e / sum) : 0.f;
+}
+
+// Pass 2: pooled_b[c] = f32(sum_t p_t x_t[c]) with f64 accumulation (predictor.py:78), p
+// from softmax_kernel.  grid (ceil(d / 512), blk_count); blocks run in reverse so the
+// rows pass 1 read last are still in L2.  Warp w covers 256 columns (8 per lane, half
+// h = w & 1 of the CTA's 512) for the 32 tokens of quarter w >> 1, with kBatch loads of
+// 16 B in flight per lane; the four quarter partials are added in order.
+// Widening: F2F (bf16 -> f32 is a shift, then one cvt per element) -- the INT-pipe
+// widening of r2 cost ~11 instructions per element and made the pass issue bound.
+#ifndef FFWD_POOL_F2F
+#define FFWD_POOL_F2F 1
+#endif
 template <bool kF32>
 __global__ void __launch_bounds__(kPoolThreads, FFWD_POOL_MINB)
     pooled_kernel(const void* __restrict__ x, int T, int d, int blk_begin, int blk_count,
-                  const float* __restrict__ logits, float* __restrict__ pooled) {
+                  const float* __restrict__ probs, float* __restrict__ pooled) {
   __shared__ double probd[kBlockTokens];
-  __shared__ double wred[2][4];
   __shared__ double red[kPoolQuarters][kPoolCols];
   pdl_wait();
   pdl_trigger();
@@ -192,26 +222,10 @@ __global__ void __launch_bounds__(kPoolThreads, FFWD_POOL_MINB)
   const int tok0 = (blk_begin + rel) * kBlockTokens;
   const int n = min(kBlockTokens, T - tok0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // ---- softmax over the block's logits (f64, max-subtracted), rounded to f32
-  const double l = threadIdx.x < n ? static_cast<double>(logits[rel * kBlockTokens + threadIdx.x])
-                                   : -INFINITY;
-  const double wm = warp_max_f64(l);
-  if (warp < 4 && lane == 0) wred[0][warp] = wm;
-  __syncthreads();
-  const double m = fmax(fmax(wred[0][0], wred[0][1]), fmax(wred[0][2], wred[0][3]));
-  const double e = threadIdx.x < n ? exp(l - m) : 0.0;
-  const double ws = warp_sum_f64(e);
-  if (warp < 4 && lane == 0) wred[1][warp] = ws;
-  __syncthreads();
-  if (threadIdx.x < kBlockTokens) {
-    const double sum = ((wred[1][0] + wred[1][1]) + wred[1][2]) + wred[1][3];
-    probd[threadIdx.x] =
-        threadIdx.x < n ? static_cast<double>(static_cast<float>(e / sum)) : 0.0;
-  }
+  if (threadIdx.x < kBlockTokens)
+    probd[threadIdx.x] = static_cast<double>(probs[rel * kBlockTokens + threadIdx.x]);
   __syncthreads();
 
-  // ---- pooled partials
   const int half = warp & 1, quarter = warp >> 1;
   const int cl = half * 256 + lane * 8;  // column within the CTA's 512
   const int c = blockIdx.x * kPoolCols + cl;
@@ -229,8 +243,8 @@ __global__ void __launch_bounds__(kPoolThreads, FFWD_POOL_MINB)
         if (t0 + u < n) xr[u].load(x, static_cast<size_t>(tok0 + t0 + u) * d + c);
         else xr[u].zero();
       }
-      bool special = false;  // bf16: widen on the INT pipe unless a lane holds 0/subnormal/inf/NaN
-      if constexpr (!kF32) {
+      bool special = false;  // INT-pipe widening unless a lane holds 0/subnormal/inf/NaN
+      if constexpr (!kF32 && !FFWD_POOL_F2F) {
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
           const uint32_t* w = reinterpret_cast<const uint32_t*>(xr[u].v);
@@ -238,7 +252,7 @@ __global__ void __launch_bounds__(kPoolThreads, FFWD_POOL_MINB)
           for (int q = 0; q < 4; ++q) special |= widen::bf16x2_special(w[q]);
         }
       }
-      if (kF32 || __any_sync(__activemask(), special)) {
+      if (kF32 || FFWD_POOL_F2F || __any_sync(__activemask(), special)) {
 #pragma unroll
         for (int u = 0; u < kBatch; ++u) {
           const double pt = probd[t0 + u];
@@ -586,7 +600,7 @@ int gemm_splits(int M, int K, int N) {
 
 cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begin, int blk_count,
                         const float* query, float sqrt_d, float* logits, float* pooled,
-                        const float* logits_in, cudaStream_t s) {
+                        const float* logits_in, float* probs, cudaStream_t s) {
   if (blk_count <= 0) return cudaSuccess;
   const int tok0 = blk_begin * kBlockTokens;
   const int ntok = std::min(T, (blk_begin + blk_count) * kBlockTokens) - tok0;
@@ -594,22 +608,19 @@ cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begi
   // logits_in: precomputed by the producer of X (absolute token index), e.g. the fused
   // RMSNorm; the first pass is then skipped.
   const float* lg = logits_in ? logits_in + tok0 : logits;
-  if (x_is_f32) {
-    if (!logits_in) {
-      cudaError_t e = launch_logits<true>(x, d, tok0, ntok, query, sqrt_d, logits, s);
-      if (e != cudaSuccess) return e;
-    }
-    return launch_k(pooled_kernel<true>, g2, dim3(kPoolThreads), 0, s, 1, x, T, d, blk_begin,
-                    blk_count, lg, pooled);
-  } else {
-    if (!logits_in) {
-      cudaError_t e = launch_logits<false>(x, d, tok0, ntok, query, sqrt_d, logits, s);
-      if (e != cudaSuccess) return e;
-    }
-    return launch_k(pooled_kernel<false>, g2, dim3(kPoolThreads), 0, s, 1, x, T, d, blk_begin,
-                    blk_count, lg, pooled);
+  if (!logits_in) {
+    cudaError_t e = x_is_f32 ? launch_logits<true>(x, d, tok0, ntok, query, sqrt_d, logits, s)
+                             : launch_logits<false>(x, d, tok0, ntok, query, sqrt_d, logits, s);
+    if (e != cudaSuccess) return e;
   }
-  return cudaGetLastError();
+  cudaError_t e = launch_k(softmax_kernel, dim3(blk_count), dim3(kBlockTokens), 0, s, 1, T,
+                           blk_begin, lg, probs);
+  if (e != cudaSuccess) return e;
+  if (x_is_f32)
+    return launch_k(pooled_kernel<true>, g2, dim3(kPoolThreads), 0, s, 1, x, T, d, blk_begin,
+                    blk_count, static_cast<const float*>(probs), pooled);
+  return launch_k(pooled_kernel<false>, g2, dim3(kPoolThreads), 0, s, 1, x, T, d, blk_begin,
+                  blk_count, static_cast<const float*>(probs), pooled);
 }
 
 cudaError_t launch_pool_generic(const void* x, bool x_is_f32, int T, int d, int rpb,

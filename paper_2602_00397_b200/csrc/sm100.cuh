@@ -109,6 +109,23 @@ __device__ __forceinline__ void tma_gather4(const CUtensorMap* m, uint64_t* bar,
       : "memory");
 }
 
+// 1-D bulk copy global -> shared (TMA, no tensor map): `bytes` (multiple of 16, both
+// addresses 16 B aligned), completion counted on `bar` as transaction bytes.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Order this thread's generic-proxy shared-memory accesses before later async-proxy
+// (TMA) accesses of the same buffer (a refill after the consumer wrote into it).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // L2 prefetch of four arbitrary rows (tile::gather4 addressing, no shared-memory
 // destination, no barrier): warms L2 with a later stage's gathered rows.
 __device__ __forceinline__ void tma_prefetch_gather4(const CUtensorMap* m, int32_t c0, int32_t r0,
