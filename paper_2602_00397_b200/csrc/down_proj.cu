@@ -38,6 +38,10 @@
 #define FFWD_STAGES_A FFWD_DOWN_STAGES_A
 #define FFWD_STAGES_B FFWD_DOWN_STAGES_B
 #endif
+// FFWD_K3_A_LDGSTS: H tiles by cp.async from the A-loader warp instead of TMA boxes
+#ifdef FFWD_K3_A_LDGSTS
+#define FFWD_A_LDGSTS
+#endif
 #include "gemm_sm100.cuh"
 #include "launch.cuh"
 
@@ -63,6 +67,9 @@
 namespace ffwd {
 
 namespace {
+#ifdef FFWD_PROBE
+__device__ unsigned long long g_probe_down[256][5];  // per CTA: wait A, wait B, wait TMEM, total, stages
+#endif
 
 using namespace gemm;
 
@@ -199,6 +206,38 @@ __global__ void __launch_bounds__(kThreads, 1)
         advance(stage, phase);
       }
     }
+  } else if (kSplit && kALdgsts && warp == kAWarp) {
+    // ---------------- A loader, LSU path: the block's H tile by 16 B cp.async, written in
+    // the 128B-swizzled K-major layout the UMMA descriptor expects (16 B chunk c of row r
+    // at r * 128 + ((c ^ (r & 7)) * 16))
+    uint32_t sa = 0, pa = 0;
+    const __nv_bfloat16* H = static_cast<const __nv_bfloat16*>(a.h);
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const Tile tl = a.down_tiles[t];
+      if (tl.b < 0) continue;
+      const int nk = a.meta[tl.b].ktot / BK;
+      if (a.blk_done) {
+        if (lane == 0) wait_block_h(a.blk_done + tl.b, a.meta[tl.b].n_up);
+        __syncwarp();
+      }
+      const __nv_bfloat16* hb = H + static_cast<size_t>(tl.b) * kBlockTokens * a.hcols;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&sm.bar->emptyA[sa], pa ^ 1);
+        const int kr = tl.pad ? nk - 1 - kb : kb;
+        uint8_t* dst = sm.a_stage(sa);
+#pragma unroll 8
+        for (int i = 0; i < (BM * 8) / 32; ++i) {
+          const int q = static_cast<int>(lane) + 32 * i;  // 16 B chunk of the tile
+          const int r = q >> 3, c = q & 7;
+          cp_async_cg16(dst + r * 128 + ((c ^ (r & 7)) << 4),
+                        hb + static_cast<size_t>(r) * a.hcols + kr * BK + c * 8);
+        }
+        cp_async_arrive_noinc(&sm.bar->fullA[sa]);
+        advance_n<kStagesA>(sa, pa);
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
   } else if (kSplit && warp == kAWarp) {
     // ---------------- A loader (split rings): the block's H tile, one 2-D box per stage
     if (lane == 0) {
@@ -231,23 +270,40 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kMmaWarp) {
     constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, true);
     if (lane == 0) {
+      Probe pr;
+#ifdef FFWD_PROBE
+      pr.t0 = clock64();
+#endif
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
       [[maybe_unused]] uint32_t sa = 0, pa = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const Tile tl = a.down_tiles[t];
         if (tl.b < 0) continue;
         const BlockMeta m = a.meta[tl.b];
+#ifdef FFWD_PROBE
+        const unsigned long long ct = clock64();
         mbar_wait_sleep(&sm.bar->tempty[acc], acc_phase ^ 1);
+        pr.wait_t += clock64() - ct;
+#else
+        mbar_wait_sleep(&sm.bar->tempty[acc], acc_phase ^ 1);
+#endif
         tc_fence_after();
         if constexpr (kSplit)
           mma_tile_split(sm, tmem + acc * BN, m.ktot / BK, idesc, kLbo, 1024, 2048, stage, phase,
-                         sa, pa);
+                         sa, pa, &pr);
         else
           mma_tile(sm, tmem + acc * BN, m.ktot / BK, idesc, kLbo, 1024, 2048, stage, phase);
         umma_commit(&sm.bar->tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
+#ifdef FFWD_PROBE
+      if (blockIdx.x < 256) {
+        unsigned long long* o = g_probe_down[blockIdx.x];
+        o[0] = pr.wait_a; o[1] = pr.wait_b; o[2] = pr.wait_t; o[3] = clock64() - pr.t0;
+        o[4] = pr.stages;
+      }
+#endif
     }
     __syncwarp();
   } else {
@@ -367,3 +423,9 @@ cudaError_t launch_down_proj(const GemmArgs& a, cudaStream_t s) {
 }
 
 }  // namespace ffwd
+
+#ifdef FFWD_PROBE
+extern "C" __attribute__((visibility("default"))) int ffwd_probe_read_down(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, ffwd::g_probe_down, sizeof(ffwd::g_probe_down)) == cudaSuccess ? 0 : 1;
+}
+#endif

@@ -62,6 +62,16 @@ constexpr int kAWarp = kProducerWarps + 5;  // A loader (split rings only)
 constexpr int kThreads = (kProducerWarps + 5 + (kSplit ? 1 : 0)) * 32;
 static_assert(kProducerWarps % 4 == 0 && 64 % kProducerWarps == 0, "producer split");
 constexpr uint32_t kTmemCols = 512;
+// FFWD_A_LDGSTS (per kernel TU): the A tile is copied by the A-loader warp's 32 lanes with
+// 16 B cp.async (the LSU path) instead of one TMA box, so A does not queue in the SM's TMA
+// unit behind the B gathers; fullA then counts one cp.async arrival per lane.
+#ifdef FFWD_A_LDGSTS
+constexpr bool kALdgsts = true;
+constexpr uint32_t kALanes = 32;
+#else
+constexpr bool kALdgsts = false;
+constexpr uint32_t kALanes = 1;
+#endif
 constexpr int kABytes = BM * BK * 2;  // 16 KiB
 
 __host__ __device__ constexpr int round_up(int v, int m) { return (v + m - 1) / m * m; }
@@ -116,7 +126,7 @@ __device__ __forceinline__ void prologue(Smem<kBBytes>& sm, int warp) {
       mbar_init(&sm.bar->empty[i], 1);
     }
     for (int i = 0; i < kStagesA; ++i) {
-      mbar_init(&sm.bar->fullA[i], 1);
+      mbar_init(&sm.bar->fullA[i], kALanes);
       mbar_init(&sm.bar->emptyA[i], kPairA ? 2 : 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -187,14 +197,35 @@ __device__ __forceinline__ void advance(uint32_t& stage, uint32_t& phase) {
 
 // Split rings: the MMA waits for the stage's A slot and B slot separately and
 // releases both.
+// FFWD_PROBE builds (timing experiments only): the MMA thread's cycles spent waiting
+// for A and for B, accumulated per CTA.
+struct Probe {
+  unsigned long long wait_a = 0, wait_b = 0, wait_t = 0, t0 = 0, stages = 0;
+};
+
 template <int kBBytes>
 __device__ __forceinline__ void mma_tile_split(Smem<kBBytes>& sm, uint32_t tmem_d, int nk,
                                                uint32_t idesc, uint32_t b_lbo, uint32_t b_sbo,
                                                uint32_t b_kstep, uint32_t& sb, uint32_t& pb,
-                                               uint32_t& sa, uint32_t& pa) {
+                                               uint32_t& sa, uint32_t& pa,
+                                               Probe* pr = nullptr) {
   for (int kb = 0; kb < nk; ++kb) {
+#ifdef FFWD_PROBE
+    const unsigned long long c0 = clock64();
+    mbar_wait(&sm.bar->fullA[sa], pa);
+    const unsigned long long c1 = clock64();
+    mbar_wait(&sm.bar->full[sb], pb);
+    const unsigned long long c2 = clock64();
+    if (pr) {
+      pr->wait_a += c1 - c0;
+      pr->wait_b += c2 - c1;
+      pr->stages += 1;
+    }
+#else
     mbar_wait(&sm.bar->fullA[sa], pa);
     mbar_wait(&sm.bar->full[sb], pb);
+#endif
+    if constexpr (kALdgsts) fence_proxy_async_smem();  // cp.async (generic proxy) -> UMMA
     tc_fence_after();
     const uint64_t adesc = make_sdesc_sw128(smem_u32(sm.a_stage(sa)), 16, 1024);
     const uint64_t bdesc = make_sdesc_sw128(smem_u32(sm.b_stage(sb)), b_lbo, b_sbo);

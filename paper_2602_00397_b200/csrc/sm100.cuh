@@ -120,6 +120,19 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+// 16 B global -> shared copy through L2 (LDGSTS, the LSU path: not the TMA unit)
+__device__ __forceinline__ void cp_async_cg16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+
+// arrive on `bar` once all of this thread's earlier cp.async copies have landed (the
+// barrier's expected count includes this arrival: .noinc)
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
 // Order this thread's generic-proxy shared-memory accesses before later async-proxy
 // (TMA) accesses of the same buffer (a refill after the consumer wrote into it).
 __device__ __forceinline__ void fence_proxy_async_smem() {

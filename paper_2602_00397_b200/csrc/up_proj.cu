@@ -46,6 +46,9 @@
 namespace ffwd {
 
 namespace {
+#ifdef FFWD_PROBE
+__device__ unsigned long long g_probe_up[256][5];  // per CTA: wait A, wait B, wait TMEM, total, stages
+#endif
 
 using namespace gemm;
 
@@ -178,20 +181,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- MMA issuer
     constexpr uint32_t idesc = make_idesc_bf16(BM, UP_BN, false, false);
     if (lane == 0) {
+      Probe pr;
+#ifdef FFWD_PROBE
+      pr.t0 = clock64();
+#endif
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0, sa = 0, pa = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const Tile tl = a.up_tiles[t];
         if (tl.b < 0) continue;
+#ifdef FFWD_PROBE
+        const unsigned long long ct = clock64();
         mbar_wait_sleep(&sm.bar->tempty[acc], acc_phase ^ 1);
+        pr.wait_t += clock64() - ct;
+#else
+        mbar_wait_sleep(&sm.bar->tempty[acc], acc_phase ^ 1);
+#endif
         tc_fence_after();
         if constexpr (kSplit)
-          mma_tile_split(sm, tmem + acc * UP_BN, nk, idesc, 16, 1024, 32, stage, phase, sa, pa);
+          mma_tile_split(sm, tmem + acc * UP_BN, nk, idesc, 16, 1024, 32, stage, phase, sa, pa, &pr);
         else
           mma_tile(sm, tmem + acc * UP_BN, nk, idesc, 16, 1024, 32, stage, phase);
         umma_commit(&sm.bar->tfull[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
+#ifdef FFWD_PROBE
+      if (blockIdx.x < 256) {
+        unsigned long long* o = g_probe_up[blockIdx.x];
+        o[0] = pr.wait_a; o[1] = pr.wait_b; o[2] = pr.wait_t; o[3] = clock64() - pr.t0;
+        o[4] = pr.stages;
+      }
+#endif
     }
     __syncwarp();
   } else {
@@ -294,3 +314,9 @@ cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s) {
 }
 
 }  // namespace ffwd
+
+#ifdef FFWD_PROBE
+extern "C" __attribute__((visibility("default"))) int ffwd_probe_read_up(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, ffwd::g_probe_up, sizeof(ffwd::g_probe_up)) == cudaSuccess ? 0 : 1;
+}
+#endif
