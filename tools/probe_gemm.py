@@ -1,6 +1,6 @@
 """Where the gather-GEMMs' MMA thread waits (FFWD_PROBE build: tools/build_variant.sh probe
 -DFFWD_PROBE; run with FFWD_LIB=build/libffwd_probe.so).  One 8B/16K layer of the bench
-step, then per-CTA cycle counts of the last K2 and K3 launches."""
+step, then per-CTA cycle counts of the last K2 and K3 launches.  usage: probe_gemm.py [CFG] [T]"""
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -13,6 +13,8 @@ from paper_2602_00397_b200.norm import rmsnorm
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "8b"
 d, f, _, T, keep = bench.CONFIGS[cfg]
+if len(sys.argv) > 2:  # token-count override (K3 with H L2-resident at small T)
+    T = int(sys.argv[2])
 bench.CONFIGS[cfg] = (d, f, 1, T, keep)
 dev = torch.device("cuda", 0)
 layers, ks = bench.make_layers(cfg, dev, 0, 1)
@@ -34,7 +36,7 @@ for tag in ("up", "down"):
     getattr(lib, f"ffwd_probe_read_{tag}")(buf)
     a = np.frombuffer(buf, dtype=np.uint64).reshape(256, 5)[:148].astype(np.float64)
     tot = a[:, 3]
-    print(f"{tag}: total {tot.mean():.0f} cyc/CTA; MMA thread waiting on A {a[:, 0].sum() / tot.sum() * 100:.1f}%, "
+    print(f"T={T} {tag}: total {tot.mean():.0f} cyc/CTA; MMA thread waiting on A {a[:, 0].sum() / tot.sum() * 100:.1f}%, "
           f"on B {a[:, 1].sum() / tot.sum() * 100:.1f}%, on the epilogue (TMEM) {a[:, 2].sum() / tot.sum() * 100:.1f}%; "
           f"stages/CTA {a[:, 4].mean():.0f}, cycles/stage {tot.sum() / a[:, 4].sum():.0f}; "
           f"CTA total min/max {tot.min():.0f}/{tot.max():.0f}")

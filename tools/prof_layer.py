@@ -14,6 +14,8 @@ if len(sys.argv) > 5:  # serpentine 0/1
     from paper_2602_00397_b200 import _lib
     _lib.load_library().ffwd_set_serpentine(int(sys.argv[5]))
 d, f, L, T, keep = bench.CONFIGS[cfg]
+if os.environ.get("FFWD_T"):  # token-count override
+    T = int(os.environ["FFWD_T"])
 bench.CONFIGS[cfg] = (d, f, 1, T, keep)
 dev = torch.device("cuda", 0)
 layers, ks = bench.make_layers(cfg, dev, 0, 1)
