@@ -503,6 +503,8 @@ def run_gpu(args, rank: int, world: int) -> None:
         r0, r1 = seq_rows(T, rank, world)
         x0 = x0[r0:r1].contiguous()  # this rank's rows of the residual stream
         sp_tp = SeqParallelTP(layers, T, d, rank, world, dev, comm=TorchComm(), gain=gain,
+                              shard_predictor={"auto": None, "sharded": True,
+                                               "replicated": False}[args.predictor],
                               reduce_dtype=torch.bfloat16 if args.reduce_dtype == "bf16"
                               else torch.float32)
     T_loc = x0.shape[0]
@@ -724,7 +726,11 @@ def run_gpu(args, rank: int, world: int) -> None:
         "data": "synthetic (random-init normal*0.02 weights, N(0,1) bf16 hidden states)",
         "config": workload_config(args, T, L, ks, world),
         "collective": ({"rs_ag": f"NCCL all-gather x (bf16) + reduce-scatter y "
-                                  f"({args.reduce_dtype}), sequence-parallel residual",
+                                  f"({args.reduce_dtype}), sequence-parallel residual, "
+                                  + ("sequence-parallel predictor (all-gather of the "
+                                     "selection bitmasks)" if sp_tp is not None and
+                                     sp_tp.shard_predictor else "replicated predictor "
+                                     "(all-gather of the logits)"),
                         "allreduce": "NCCL all-reduce of y (f32)", "nccl": "NCCL all-reduce "
                         "of y (f32)", "fused": "peer-memory all-reduce kernel (NVLink P2P)",
                         "overlap": "peer-memory all-reduce overlapped with the down "
@@ -831,6 +837,10 @@ def main():
     ap.add_argument("--skip-ttft", action="store_true")
     ap.add_argument("--skip-f32-pred", action="store_true",
                     help="skip timing the f32-predictor-input variant")
+    ap.add_argument("--predictor", default="auto", choices=["auto", "sharded", "replicated"],
+                    help="TP with rs_ag: each rank predicts only its own blocks and the "
+                         "selection bitmasks are all-gathered (sharded; auto = from 4 ranks), "
+                         "or every rank predicts every block (replicated)")
     ap.add_argument("--collective", default="rs_ag",
                     choices=["rs_ag", "allreduce", "nccl", "fused", "overlap"],
                     help="TP completion: rs_ag = sequence-parallel residual (NCCL all-gather "

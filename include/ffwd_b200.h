@@ -222,6 +222,38 @@ FFWD_API int ffwd_ffn_layer2(const void* x_bf16, int T, int d, const void* wgu_t
                     size_t workspace_bytes, void* stream);
 
 /*
+ * The sequence-parallel predictor (tp.SeqParallelTP): under tensor parallelism each rank
+ * predicts only the blocks of its own T/N residual rows and the ranks all-gather the
+ * selections as bitmasks, instead of every rank predicting every block.
+ *
+ * ffwd_predict_mask: predictor_forward + build_mask (predictor.py:68-81,
+ * kernels.py:139-149, sparse.py:49-55) for blocks [blk_begin, blk_begin + blk_count) of
+ * x [T x d] (bf16, or f32 when x_is_f32), with the per-token logits from the FFN-input
+ * producer when logits_in (f32 [T]) is given.  Row i of `mask` (ld_mask >= ceil(f / 32)
+ * 32-bit words per row) receives block blk_begin + i's selection: bit j of word j / 32 =
+ * neuron j kept.  Bit-identical to the indices ffwd_ffn_layer2 selects for those blocks.
+ */
+FFWD_API size_t ffwd_predict_mask_workspace_bytes(int blk_count, int d, int r, int f);
+FFWD_API int ffwd_predict_mask(const void* x, int x_is_f32, int T, int d, int blk_begin,
+                               int blk_count, const float* query, const float* w1,
+                               const float* w2, int r, int f, int k, const float* logits_in,
+                               uint32_t* mask, int ld_mask, void* workspace,
+                               size_t workspace_bytes, void* stream);
+/*
+ * ffwd_ffn_layer2 with the selection given: `mask` holds one row per block of x (row b =
+ * block b; only the predicted blocks' rows are read), in the ffwd_predict_mask format.
+ * The rank keeps its own strided neurons of each row (local ids j / tp_size, ascending)
+ * and runs the gather-GEMMs and compensator exactly as ffwd_ffn_layer2.  Workspace: the
+ * ffwd_layer_workspace_bytes size suffices.
+ */
+FFWD_API int ffwd_ffn_layer_masked(const void* x_bf16, int T, int d, const void* wgu_t,
+                                   const void* wd, int f_local, int rc_local, int f_global,
+                                   int k, int dense_first_last, int has_comp, int tp_rank,
+                                   int tp_size, const uint32_t* mask, int ld_mask, float* y,
+                                   const float* residual, void* x_next_bf16, void* workspace,
+                                   size_t workspace_bytes, void* stream);
+
+/*
  * kernels.rmsnorm (kernels.py:96-106) of the f32 residual stream x [T x d]:
  * out = f32(x / sqrt(mean_f64(x^2) + eps) * gain), evaluated in f64 like the
  * reference, written to out_bf16 (bf16 [T x d]) and/or out_f32.  With `add`

@@ -18,8 +18,8 @@ from .sparse import (ExpertMask, FirstBlockStatic, SubWeights, budget_to_k, buil
 from .scheduler import (AttentionMassProfile, SparsityPlan, allocate_budgets, budgets_to_topk,
                         dense_plan, load_plan, plan_from_profile, save_plan, uniform_plan)
 from .costmodel import FlopsReport, ffn_path_flops, predict_prefill_flops
-from .layer import (PackedLayer, dense_ffn, ffn_layer_mode, invalidate_packed, oracle_scores,
-                    pack_layer,
+from .layer import (PackedLayer, dense_ffn, ffn_layer_mode, invalidate_packed, mask_indices,
+                    mask_words, oracle_scores, pack_layer, predict_mask,
                     run_sparse_ffn, seq_shard, set_raster, shard_comp_cols, shard_neurons,
                     sparse_ffn_layer)
 

@@ -47,6 +47,12 @@ SIGNATURES = {
     "ffwd_ffn_layer": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _vp, _vp, _vp,
                                 _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp,
                                 _vp, _vp, _vp, _c_int, _vp, _c_size, _vp]),
+    "ffwd_predict_mask_workspace_bytes": (_c_size, [_c_int, _c_int, _c_int, _c_int]),
+    "ffwd_predict_mask": (_c_int, [_vp, _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _vp, _vp,
+                                   _c_int, _c_int, _c_int, _vp, _vp, _c_int, _vp, _c_size, _vp]),
+    "ffwd_ffn_layer_masked": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _c_int,
+                                       _c_int, _c_int, _c_int, _c_int, _c_int, _vp, _c_int, _vp,
+                                       _vp, _vp, _vp, _c_size, _vp]),
     "ffwd_ffn_layer2": (_c_int, [_vp, _c_int, _c_int, _vp, _vp, _c_int, _c_int, _vp, _vp, _vp,
                                  _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _c_int, _vp,
                                  _vp, _vp, _vp, _c_int, _vp, _vp, _vp, _c_size, _vp]),

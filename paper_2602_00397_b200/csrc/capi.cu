@@ -572,6 +572,87 @@ int ffwd_ffn_layer2(const void* x_bf16, int T, int d, const void* wgu_t, const v
                  tp_size > 1 ? w.counts : nullptr, k, 0, has_comp, y, residual, x_next_bf16, s);
 }
 
+size_t ffwd_predict_mask_workspace_bytes(int blk_count, int d, int r, int f) {
+  Carve c(nullptr);
+  carve_pred(c, blk_count, d, r, f, true);
+  return c.off;
+}
+
+int ffwd_predict_mask(const void* x, int x_is_f32, int T, int d, int blk_begin, int blk_count,
+                      const float* query, const float* w1, const float* w2, int r, int f, int k,
+                      const float* logits_in, uint32_t* mask, int ld_mask, void* workspace,
+                      size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  int rc = check_common(T, d, f, k);
+  if (rc) return rc;
+  if (blk_count < 1 || blk_begin < 0 || (blk_begin + blk_count - 1) * kBlockTokens >= T)
+    return fail(FFWD_ERR_VALIDATION, "blocks [%d, %d) outside the %d tokens", blk_begin,
+                blk_begin + blk_count, T);
+  if (d % 8 != 0) return fail(FFWD_ERR_UNSUPPORTED, "predictor needs d_model %% 8 == 0");
+  if (ld_mask < (f + 31) / 32) return fail(FFWD_ERR_VALIDATION, "ld_mask < ceil(f / 32)");
+  if (!x || !query || !w1 || !w2 || !mask || !workspace)
+    return fail(FFWD_ERR_VALIDATION, "predict_mask: null pointer");
+  if (workspace_bytes < ffwd_predict_mask_workspace_bytes(blk_count, d, r, f))
+    return fail(FFWD_ERR_VALIDATION, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carve c(workspace);
+  Pred p = carve_pred(c, blk_count, d, r, f, true);
+  rc = run_predictor(x, x_is_f32 != 0, T, d, blk_begin, blk_count, query, w1, w2, r, f, p,
+                     p.scores, s, logits_in);
+  if (rc) return rc;
+  StageTimer tm(kTopk, s);
+  FFWD_CUDA(launch_topk(p.scores, blk_count, f, k, 0, 1, nullptr, 0, nullptr, 0, nullptr, s, mask,
+                        ld_mask),
+            "topk");
+  return FFWD_OK;
+}
+
+int ffwd_ffn_layer_masked(const void* x_bf16, int T, int d, const void* wgu_t, const void* wd,
+                          int f_local, int rc_local, int f_global, int k, int dense_first_last,
+                          int has_comp, int tp_rank, int tp_size, const uint32_t* mask,
+                          int ld_mask, float* y, const float* residual, void* x_next_bf16,
+                          void* workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  int rc = check_common(T, d, f_global, k);
+  if (rc) return rc;
+  if ((rc = check_gemm_shapes(d, f_local))) return rc;
+  if (tp_size < 1 || tp_rank < 0 || tp_rank >= tp_size)
+    return fail(FFWD_ERR_VALIDATION, "bad tensor-parallel rank %d of %d", tp_rank, tp_size);
+  if (dense_first_last < 0 || dense_first_last > 3)
+    return fail(FFWD_ERR_VALIDATION, "dense_first_last must be 0..3, got %d", dense_first_last);
+  if (f_local != (f_global - tp_rank + tp_size - 1) / tp_size)
+    return fail(FFWD_ERR_VALIDATION, "f_local=%d is not rank %d's strided share of d_ffn=%d",
+                f_local, tp_rank, f_global);
+  if (has_comp && rc_local < 1) return fail(FFWD_ERR_VALIDATION, "compensator width must be >= 1");
+  if (residual && tp_size != 1)
+    return fail(FFWD_ERR_VALIDATION, "fused residual needs tp_size == 1 (reduce the partials first)");
+  if (!x_bf16 || !wgu_t || !wd || !workspace || (!y && !x_next_bf16))
+    return fail(FFWD_ERR_VALIDATION, "ffn_layer: null x, weight, output or workspace pointer");
+  if (!y && residual)
+    return fail(FFWD_ERR_VALIDATION, "ffn_layer: the residual add needs the f32 output y");
+  int b0, nb;
+  layer_split(T, k, f_global, dense_first_last, &b0, &nb);
+  if (nb > 0 && (!mask || ld_mask < (f_global + 31) / 32))
+    return fail(FFWD_ERR_VALIDATION, "ffn_layer_masked: predicted blocks need mask rows of "
+                "ceil(d_ffn / 32) words");
+  const int kmax = local_kmax(k, f_local);
+  Carve c0(nullptr);
+  carve_ffn(c0, T, d, f_local, rc_local, kmax, nb, rup(kmax, 4));
+  if (workspace_bytes < c0.off) return fail(FFWD_ERR_VALIDATION, "workspace too small");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carve c(workspace);
+  Ffn w = carve_ffn(c, T, d, f_local, rc_local, kmax, nb, rup(kmax, 4));
+  if (nb > 0) {
+    StageTimer tm(kTopk, s);
+    FFWD_CUDA(launch_mask_to_local(mask + static_cast<size_t>(b0) * ld_mask, ld_mask, nb,
+                                   f_global, tp_rank, tp_size, w.idx_local, w.ld_local, w.counts,
+                                   s),
+              "mask_to_local");
+  }
+  return run_ffn(x_bf16, T, d, wgu_t, wd, f_local, rc_local, w, w.idx_local, w.ld_local, b0, nb,
+                 w.counts, k, 0, has_comp, y, residual, x_next_bf16, s);
+}
+
 int ffwd_ffn_layer(const void* x_bf16, int T, int d, const void* wgu_t, const void* wd,
                    int f_local, int rc_local, const float* query, const float* w1,
                    const float* w2, int r, int f_global, int k, int dense_first_last,

@@ -87,9 +87,15 @@ cudaError_t launch_rope(void* qk, bool is_f32, int T, int row_stride, int k_col,
 size_t gemm_f64acc_partial_bytes(int M, int K, int N);
 cudaError_t launch_gemm_f64acc(const float* A, const float* B, float* C, int M, int K, int N,
                                bool relu, double* partial, cudaStream_t s);
+// `mask` (nullable): also the selection bitmask of each row (ld_mask 32-bit words per row)
 cudaError_t launch_topk(const float* scores, int n_rows, int f, int k, int tp_rank, int tp_size,
                         int32_t* idx_global, int ld_global, int32_t* idx_local, int ld_local,
-                        int32_t* counts, cudaStream_t s);
+                        int32_t* counts, cudaStream_t s, uint32_t* mask = nullptr,
+                        int ld_mask = 0);
+// rank tp_rank's local neuron lists + counts from selection bitmasks (rows of ld_mask words)
+cudaError_t launch_mask_to_local(const uint32_t* mask, int ld_mask, int n_rows, int f_global,
+                                 int tp_rank, int tp_size, int32_t* idx_local, int ld_local,
+                                 int32_t* counts, cudaStream_t s);
 
 // ------------------------------------------------------------------ K2/K3
 struct PlanArgs {

@@ -69,11 +69,14 @@ constexpr int kBinsPerThread = kBins / kTopkThreads;  // 4
 
 // kCached: the row's keys are staged once in shared memory (f * 4 bytes), else every
 // pass re-reads the scores (from L2) -- only for very wide rows.
+// `mask` (nullable): the row's selection as a bitmask (bit j of word j / 32 = neuron j
+// kept), `ld_mask` words per row -- the compact form the sequence-parallel predictor
+// all-gathers between tensor-parallel ranks (tp.SeqParallelTP).
 template <bool kCached>
 __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
     const float* __restrict__ scores, int f, int k, int tp_rank, int tp_size,
     int32_t* __restrict__ idx_global, int ld_global, int32_t* __restrict__ idx_local,
-    int ld_local, int32_t* __restrict__ counts) {
+    int ld_local, int32_t* __restrict__ counts, uint32_t* __restrict__ mask, int ld_mask) {
   extern __shared__ uint32_t s_keys[];
   __shared__ int hist[kBins];
   __shared__ int warp_tot[32];
@@ -186,6 +189,12 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
   const int pos = block_exclusive_scan(kept, warp_tot, &s_total);
   const int pos_loc = block_exclusive_scan(kept_loc, warp_tot, &s_total);
   if (tid == kTopkThreads - 1 && counts != nullptr) counts[blockIdx.x] = pos_loc + kept_loc;
+  const int nw = (f + 31) / 32;
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(hist);  // the histogram is done with
+  if (mask) {
+    for (int i = tid; i < nw; i += kTopkThreads) s_mask[i] = 0u;
+    __syncthreads();
+  }
   int p = pos, pl = pos_loc, te = take_eq;
   for (int i = lo; i < hi; ++i) {
     const uint32_t key = key_at(i);
@@ -195,12 +204,73 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
       --te;
     }
     if (!keep) continue;
+    if (mask) atomicOr(&s_mask[i >> 5], 1u << (i & 31));
     if (idx_global) idx_global[static_cast<size_t>(blockIdx.x) * ld_global + p] = i;
     ++p;
     if (tp1 || (i % tp_size) == tp_rank) {  // tp1: skip the integer divisions
       if (idx_local)
         idx_local[static_cast<size_t>(blockIdx.x) * ld_local + pl] = tp1 ? i : i / tp_size;
       ++pl;
+    }
+  }
+  if (mask) {
+    __syncthreads();
+    uint32_t* out = mask + static_cast<size_t>(blockIdx.x) * ld_mask;
+    for (int i = tid; i < nw; i += kTopkThreads) out[i] = s_mask[i];
+  }
+}
+
+// One rank's neuron list from a selection bitmask (the sequence-parallel predictor's
+// exchange format): row r's local ids u (ascending) with bit tp_rank + tp_size u set, and
+// their count -- exactly what topk_kernel writes as idx_local / counts for that rank.
+// Thread t owns a contiguous run of "local words" (32 consecutive local ids each, built
+// from the strided global bits), so the count is a popcount and the ids come out of the
+// set bits in order.
+constexpr int kMaskWordsPerThread = 4;
+__global__ void __launch_bounds__(kTopkThreads) mask_to_local_kernel(
+    const uint32_t* __restrict__ mask, int ld_mask, int f_global, int tp_rank, int tp_size,
+    int32_t* __restrict__ idx_local, int ld_local, int32_t* __restrict__ counts) {
+  __shared__ int warp_tot[32];
+  __shared__ int s_total;
+  pdl_wait();
+  pdl_trigger();
+  const uint32_t* m = mask + static_cast<size_t>(blockIdx.x) * ld_mask;
+  const int tid = threadIdx.x;
+  const int f_local = (f_global - tp_rank + tp_size - 1) / tp_size;
+  const int nlw = (f_local + 31) / 32;
+  uint32_t w[kMaskWordsPerThread];
+  int n = 0;
+#pragma unroll
+  for (int q = 0; q < kMaskWordsPerThread; ++q) {
+    const int lw = tid * kMaskWordsPerThread + q;
+    uint32_t v = 0;
+    if (lw < nlw) {
+      if (tp_size == 1) {
+        v = __ldg(m + lw);
+      } else {
+        for (int i = 0; i < 32; ++i) {
+          const int u = 32 * lw + i;
+          if (u >= f_local) break;
+          const int j = tp_rank + tp_size * u;
+          v |= ((__ldg(m + (j >> 5)) >> (j & 31)) & 1u) << i;
+        }
+      }
+      if (32 * lw + 32 > f_local) v &= (f_local - 32 * lw >= 32) ? ~0u : ((1u << (f_local - 32 * lw)) - 1u);
+    }
+    w[q] = v;
+    n += __popc(v);
+  }
+  int p = block_exclusive_scan(n, warp_tot, &s_total);
+  if (tid == kTopkThreads - 1 && counts) counts[blockIdx.x] = p + n;
+  int32_t* out = idx_local + static_cast<size_t>(blockIdx.x) * ld_local;
+#pragma unroll
+  for (int q = 0; q < kMaskWordsPerThread; ++q) {
+    uint32_t v = w[q];
+    const int base = 32 * (tid * kMaskWordsPerThread + q);
+    while (v) {
+      const int i = __ffs(v) - 1;
+      out[p++] = base + i;
+      v &= v - 1;
     }
   }
 }
@@ -211,7 +281,8 @@ constexpr size_t kTopkMaxSmem = 200 * 1024;
 
 cudaError_t launch_topk(const float* scores, int n_rows, int f, int k, int tp_rank, int tp_size,
                         int32_t* idx_global, int ld_global, int32_t* idx_local, int ld_local,
-                        int32_t* counts, cudaStream_t s) {
+                        int32_t* counts, cudaStream_t s, uint32_t* mask, int ld_mask) {
+  if (mask && (f + 31) / 32 > kBins) return cudaErrorInvalidValue;
   if (n_rows <= 0) return cudaSuccess;
   const size_t smem = static_cast<size_t>(f) * sizeof(uint32_t);
   if (smem <= kTopkMaxSmem) {
@@ -220,12 +291,24 @@ cudaError_t launch_topk(const float* scores, int n_rows, int f, int k, int tp_ra
         e != cudaSuccess)
       return e;
     return launch_k(topk_kernel<true>, dim3(n_rows), dim3(kTopkThreads), smem, s, 1, scores, f,
-                    k, tp_rank, tp_size, idx_global, ld_global, idx_local, ld_local, counts);
+                    k, tp_rank, tp_size, idx_global, ld_global, idx_local, ld_local, counts, mask,
+                    ld_mask);
   } else {
     return launch_k(topk_kernel<false>, dim3(n_rows), dim3(kTopkThreads), 0, s, 1, scores, f,
-                    k, tp_rank, tp_size, idx_global, ld_global, idx_local, ld_local, counts);
+                    k, tp_rank, tp_size, idx_global, ld_global, idx_local, ld_local, counts, mask,
+                    ld_mask);
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_mask_to_local(const uint32_t* mask, int ld_mask, int n_rows, int f_global,
+                                 int tp_rank, int tp_size, int32_t* idx_local, int ld_local,
+                                 int32_t* counts, cudaStream_t s) {
+  if (n_rows <= 0) return cudaSuccess;
+  const int f_local = (f_global - tp_rank + tp_size - 1) / tp_size;
+  if ((f_local + 31) / 32 > kTopkThreads * kMaskWordsPerThread) return cudaErrorInvalidValue;
+  return launch_k(mask_to_local_kernel, dim3(n_rows), dim3(kTopkThreads), 0, s, 1, mask, ld_mask,
+                  f_global, tp_rank, tp_size, idx_local, ld_local, counts);
 }
 
 }  // namespace ffwd

@@ -241,7 +241,8 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
                      workspace: torch.Tensor | None = None,
                      residual: torch.Tensor | None = None, x_next: torch.Tensor | None = None,
                      x_pred_f32: torch.Tensor | None = None,
-                     logits_in: torch.Tensor | None = None, f32_out: bool = True):
+                     logits_in: torch.Tensor | None = None, f32_out: bool = True,
+                     mask_in: torch.Tensor | None = None):
     """One layer's FFN branch over every block of x (T, d); returns y (T, d) f32.
 
     Semantics of ``engine.py:254-310`` (mode "predicted"): blocks 0 and n-1 run
@@ -260,6 +261,10 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
     (``norm.rmsnorm(..., predictor=...)``), which skips the pooling's first pass.
     ``f32_out=False`` writes only the bf16 ``x_next`` (no f32 y; returned in its place):
     a tensor-parallel partial for a bf16 reduce-scatter.
+    ``mask_in`` (int32 (n_blk, ceil(d_ffn / 32)) selection bitmasks, row b = block b, as
+    ``predict_mask`` writes them) gives the selection instead of running the predictor:
+    the sequence-parallel predictor under tensor parallelism (``tp.SeqParallelTP``), where
+    each rank predicts its own blocks and the masks are all-gathered.
     """
     dev = packed.device
     if packed.d != packed.d_model:
@@ -292,10 +297,23 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
     ws = workspace if workspace is not None and workspace.numel() >= ws_n else \
         _dev.workspace(dev, ws_n)
     for name, t, shape, dt in (("x_pred_f32", x_pred_f32, (T, d), torch.float32),
-                               ("logits_in", logits_in, (T,), torch.float32)):
+                               ("logits_in", logits_in, (T,), torch.float32),
+                               ("mask_in", mask_in, (n_blk, mask_words(packed.f_global)),
+                                torch.int32)):
         if t is not None and (not t.is_cuda or t.dtype != dt or tuple(t.shape) != shape
                               or not t.is_contiguous()):
             raise ValidationError(f"{name} must be a contiguous CUDA {dt} tensor of shape {shape}")
+    if mask_in is not None:
+        if return_indices or x_pred_f32 is not None or logits_in is not None:
+            raise ValidationError("mask_in replaces the predictor: no return_indices, "
+                                  "x_pred_f32 or logits_in")
+        _lib.check(lib.ffwd_ffn_layer_masked(
+            xb.data_ptr(), T, d, packed.wgu_t.data_ptr(), packed.wd.data_ptr(), packed.f_local,
+            packed.rc_local, packed.f_global, k, dfl, int(has_comp and packed.rc_local > 0),
+            packed.tp_rank, packed.tp_size, mask_in.data_ptr(), mask_in.shape[1], _dev.ptr(y),
+            _dev.ptr(residual), _dev.ptr(x_next), ws.data_ptr(), ws.numel(),
+            _dev.stream_handle(dev)), "ffn_layer_masked")
+        return y if y is not None else x_next
     _lib.check(lib.ffwd_ffn_layer2(
         xb.data_ptr(), T, d, packed.wgu_t.data_ptr(), packed.wd.data_ptr(), packed.f_local,
         packed.rc_local, predictor.query.data_ptr(), predictor.w1.data_ptr(),
@@ -309,6 +327,61 @@ def sparse_ffn_layer(x, packed: PackedLayer, predictor: DevicePredictor, k: int,
     if return_indices:
         return y, idx
     return y
+
+
+def mask_words(f: int) -> int:
+    """32-bit words per selection bitmask row of d_ffn = f neurons."""
+    return (f + 31) // 32
+
+
+def predict_mask(x, predictor: DevicePredictor, k: int, blk_begin: int = 0,
+                 blk_count: int | None = None, logits_in: torch.Tensor | None = None,
+                 out: torch.Tensor | None = None,
+                 workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Predictor + top-k of blocks [blk_begin, blk_begin + blk_count) of x (T, d) (bf16, or
+    f32 for the reference's f32 predictor input), as selection bitmasks: int32
+    (blk_count, ceil(d_ffn / 32)), bit j of word j // 32 = neuron j kept
+    (``predictor.py:68-81`` -> ``build_mask``).  ``logits_in`` (f32 (T,)): the per-token
+    logits from the FFN-input producer.  The indices are bit-identical to the ones
+    ``sparse_ffn_layer`` selects for those blocks; the masks feed its ``mask_in``."""
+    dev = predictor.w1.device
+    xt = x if isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.float32 \
+        else _x_bf16(x, dev)
+    xt = xt.contiguous()
+    T, d = xt.shape
+    if d != predictor.d:
+        raise ValidationError(f"x width {d} != predictor d_model {predictor.d}")
+    n_blk = -(-T // BLOCK)
+    if blk_count is None:
+        blk_count = n_blk - blk_begin
+    if not 1 <= k <= predictor.f:
+        raise ValidationError(f"k={k} out of range [1, {predictor.f}]")
+    w = mask_words(predictor.f)
+    if out is None:
+        out = torch.empty((blk_count, w), dtype=torch.int32, device=dev)
+    if (not out.is_cuda or out.dtype != torch.int32 or out.dim() != 2 or out.shape[0] < blk_count
+            or out.shape[1] != w or not out.is_contiguous()):
+        raise ValidationError(f"out must be a contiguous CUDA int32 tensor of {blk_count} x {w}")
+    if logits_in is not None and (not logits_in.is_cuda or logits_in.dtype != torch.float32
+                                  or tuple(logits_in.shape) != (T,)):
+        raise ValidationError(f"logits_in must be a CUDA float32 tensor of shape ({T},)")
+    lib = _dev.lib_for(dev)
+    ws_n = int(lib.ffwd_predict_mask_workspace_bytes(blk_count, d, predictor.r, predictor.f))
+    ws = workspace if workspace is not None and workspace.numel() >= ws_n else \
+        _dev.workspace(dev, ws_n)
+    _lib.check(lib.ffwd_predict_mask(
+        xt.data_ptr(), int(xt.dtype == torch.float32), T, d, blk_begin, blk_count,
+        predictor.query.data_ptr(), predictor.w1.data_ptr(), predictor.w2.data_ptr(),
+        predictor.r, predictor.f, k, _dev.ptr(logits_in), out.data_ptr(), w, ws.data_ptr(),
+        ws.numel(), _dev.stream_handle(dev)), "predict_mask")
+    return out
+
+
+def mask_indices(mask: torch.Tensor, f: int) -> list:
+    """Host helper: the ascending neuron ids of each bitmask row (int32 (n, ceil(f/32)))."""
+    m = mask.cpu().numpy().view(np.uint32)
+    bits = np.unpackbits(m.view(np.uint8), axis=1, bitorder="little")[:, :f]
+    return [np.flatnonzero(row).astype(np.int64) for row in bits]
 
 
 MODES = ("predicted", "oracle", "static")

@@ -27,7 +27,8 @@ from . import _dev, _lib
 from .compensator import CompensatorParams
 from .errors import ValidationError
 from .layer import (BLOCK, PackedLayer, dense_first_last_code, layer_workspace_bytes,
-                    pack_layer, shard_comp_cols, shard_neurons, sparse_ffn_layer)
+                    mask_words, pack_layer, predict_mask, shard_comp_cols, shard_neurons,
+                    sparse_ffn_layer)
 from .predictor import DevicePredictor
 
 
@@ -305,27 +306,36 @@ class SeqParallelTP:
       1. ``norm``: h[R_r] += y[R_r] (the previous layer's reduced FFN output,
          ``engine.py:308``) and x[R_r] = rmsnorm(h[R_r]) with the predictor's per-token
          logits -- one kernel (``ffwd_rmsnorm_ex`` with ``add``) on T/N rows;
-      2. ``gather``: all-gather x (bf16 [T x d]) and the logits (f32 [T]);
-      3. ``ffn``: the FFN branch over all T tokens on this rank's shard: the replicated
-         predictor gives every rank the same global top-k (bit-exact), each keeps its own
-         neurons -> partial y (f32, or bf16 with ``reduce_dtype=torch.bfloat16``);
-      4. ``scatter``: reduce-scatter the partial y -> y[R_r].
+      2. ``predict`` (sequence-parallel predictor, when T/N is a whole number of 128-token
+         blocks): the predictor and top-k of this rank's own blocks only
+         (``predictor.py:68-81`` is block-local), written as selection bitmasks
+         (``layer.predict_mask``: ceil(d_ffn / 32) words per block);
+      3. ``gather``: all-gather x (bf16 [T x d]) and the bitmasks ([n_blk x words]), or,
+         with a replicated predictor, x and the f32 logits;
+      4. ``ffn``: the FFN branch over all T tokens on this rank's shard: each rank keeps its
+         own neurons of every block's selection (``mask_in``; replicated predictor: every
+         rank recomputes the same global top-k, bit-exact) -> partial y (f32, or bf16 with
+         ``reduce_dtype=torch.bfloat16``);
+      5. ``scatter``: reduce-scatter the partial y -> y[R_r].
 
     ``finish`` adds the last layer's y.  NVLink bytes per rank and layer:
     (N-1)/N T d (2 + 4) (bf16 all-gather + f32 reduce-scatter; 2 + 2 with a bf16 reduce)
-    against (N-1)/N T d 8 for an f32 all-reduce, and the norm and the logits run on T/N
-    rows instead of T.
+    plus n_blk d_ffn / 8 bytes of bitmasks, against (N-1)/N T d 8 for an f32 all-reduce;
+    the norm, the logits and the predictor run on T/N rows instead of T.
 
     The phases are separate methods so a single process can drive N emulated ranks in
     lockstep (tests); ``layer`` runs them with the real collectives.  ``norm_fn`` /
-    ``ffn_fn`` replace the GPU kernels (CPU tests: the oracle)."""
+    ``predict_fn`` / ``ffn_fn`` replace the GPU kernels (CPU tests: the oracle);
+    ``ffn_fn(l, x_full, sel_full, y_part)`` gets the gathered bitmasks (sharded predictor)
+    or logits (replicated)."""
 
     def __init__(self, layers, T: int, d: int, rank: int, world: int, device,
                  comm=None, gain=None, reduce_dtype=torch.float32, dense_first_last=True,
-                 norm_fn=None, ffn_fn=None, x_dtype=torch.bfloat16):
+                 norm_fn=None, ffn_fn=None, x_dtype=torch.bfloat16, predict_fn=None,
+                 shard_predictor=None, f: int | None = None):
         if reduce_dtype not in (torch.float32, torch.bfloat16):
             raise ValidationError("reduce_dtype must be float32 or bfloat16")
-        self.layers = layers  # [(packed shard, DevicePredictor, k)]
+        self.layers = layers  # [(packed shard, DevicePredictor, k)] (CPU tests: (None, None, k))
         self.T, self.d, self.rank, self.world = T, d, rank, world
         self.r0, self.r1 = seq_rows(T, rank, world)
         dev = torch.device(device)
@@ -343,10 +353,40 @@ class SeqParallelTP:
         self.lg_full = torch.empty((T,), dtype=torch.float32, device=dev)
         self.y_part = torch.empty((T, d), dtype=reduce_dtype, device=dev)
         self.y_shard = torch.empty((n, d), dtype=reduce_dtype, device=dev)
+        # sequence-parallel predictor: this rank's rows must be whole blocks.  Default: on
+        # from 4 ranks, where the replicated predictor's share of a rank's layer is
+        # largest (single-GPU proxy, tools/tp_rank_proxy.py: -4% at TP=4, -8% at TP=8)
+        whole = T % (BLOCK * world) == 0
+        if shard_predictor and not whole:
+            raise ValidationError(f"a sharded predictor needs T % (128 x {world}) == 0, T={T}")
+        self.shard_predictor = (whole and world >= 4) if shard_predictor is None \
+            else bool(shard_predictor)
+        self.n_blk = -(-T // BLOCK)
+        if f is None:
+            f = next((lay[1].f for lay in layers if lay is not None and lay[1] is not None), None)
+        if self.shard_predictor:
+            if f is None:
+                raise ValidationError("the sharded predictor needs d_ffn (f)")
+            w = mask_words(f)
+            self.mask_shard = torch.zeros((self.n_blk // world, w), dtype=torch.int32, device=dev)
+            self.mask_full = torch.zeros((self.n_blk, w), dtype=torch.int32, device=dev)
+        self.f = f
         self.norm_fn = norm_fn or self._gpu_norm
+        self.predict_fn = predict_fn or self._gpu_predict
         self.ffn_fn = ffn_fn or self._gpu_ffn
         self.workspace = None
         self.pending = False  # y_shard holds a layer output not yet added to h
+
+    # -- which of this rank's blocks run the predictor (engine.py:258-262, :268)
+    def predicted_blocks(self, k: int) -> tuple[int, int]:
+        """Shard-relative block range [lo, hi) of this rank's predicted blocks."""
+        nbr = self.n_blk // self.world
+        if self.f is not None and k >= self.f:
+            return 0, 0  # full-K shortcut: every block dense
+        g0, g1 = self.rank * nbr, (self.rank + 1) * nbr
+        if dense_first_last_code(self.dense_first_last):
+            g0, g1 = max(g0, 1), min(g1, self.n_blk - 1)
+        return (g0 - self.rank * nbr, g1 - self.rank * nbr) if g1 > g0 else (0, 0)
 
     # -- default (GPU) compute
     def _gpu_norm(self, l, h_shard, add):
@@ -354,31 +394,48 @@ class SeqParallelTP:
         rmsnorm(h_shard, self.gain, out=self.x_shard, predictor=self.layers[l][1],
                 logits=self.lg_shard, add=add)
 
-    def _gpu_ffn(self, l, x_full, lg_full, y_part):
+    def _gpu_predict(self, l, lo, hi):
+        _, dp, k = self.layers[l]
+        predict_mask(self.x_shard, dp, k, blk_begin=lo, blk_count=hi - lo,
+                     logits_in=self.lg_shard, out=self.mask_shard[lo:hi])
+
+    def _gpu_ffn(self, l, x_full, sel_full, y_part):
         packed, dp, k = self.layers[l]
         if self.workspace is None:
             n = max(layer_workspace_bytes(self.T, p, q.r, kk, self.dense_first_last)
                     for p, q, kk in self.layers)
             self.workspace = torch.empty(n, dtype=torch.uint8, device=self.dev)
+        sel = ({"mask_in": sel_full} if self.shard_predictor else {"logits_in": sel_full})
         if y_part.dtype == torch.float32:
-            sparse_ffn_layer(x_full, packed, dp, k, out=y_part, logits_in=lg_full,
-                             workspace=self.workspace, dense_first_last=self.dense_first_last)
+            sparse_ffn_layer(x_full, packed, dp, k, out=y_part, workspace=self.workspace,
+                             dense_first_last=self.dense_first_last, **sel)
         else:
             sparse_ffn_layer(x_full, packed, dp, k, x_next=y_part, f32_out=False,
-                             logits_in=lg_full, workspace=self.workspace,
-                             dense_first_last=self.dense_first_last)
+                             workspace=self.workspace, dense_first_last=self.dense_first_last,
+                             **sel)
 
     # -- phases
     def norm(self, l: int, h_shard: torch.Tensor) -> None:
         self.norm_fn(l, h_shard, self.y_shard if self.pending else None)
         self.pending = False
 
+    def predict(self, l: int) -> None:
+        if not self.shard_predictor:
+            return
+        lo, hi = self.predicted_blocks(self.layers[l][2])
+        if hi > lo:
+            self.predict_fn(l, lo, hi)
+
     def gather(self) -> None:
         self.comm.all_gather(self.x_full, self.x_shard)
-        self.comm.all_gather(self.lg_full, self.lg_shard)
+        if self.shard_predictor:
+            self.comm.all_gather(self.mask_full, self.mask_shard)
+        else:
+            self.comm.all_gather(self.lg_full, self.lg_shard)
 
     def ffn(self, l: int) -> None:
-        self.ffn_fn(l, self.x_full, self.lg_full, self.y_part)
+        self.ffn_fn(l, self.x_full, self.mask_full if self.shard_predictor else self.lg_full,
+                    self.y_part)
 
     def scatter(self) -> None:
         self.comm.reduce_scatter(self.y_shard, self.y_part)
@@ -392,6 +449,7 @@ class SeqParallelTP:
 
     def layer(self, l: int, h_shard: torch.Tensor) -> None:
         self.norm(l, h_shard)
+        self.predict(l)
         self.gather()
         self.ffn(l)
         self.scatter()

@@ -77,13 +77,15 @@ def test_dense_first_last_codes(ff):
         ff.sparse_ffn_layer(x, packed, dp, k, dense_first_last="middle")
 
 
-@pytest.mark.parametrize("parallel", [None, "sp", "dp"])
+@pytest.mark.parametrize("parallel", [None, "sharded", "sp", "dp"])
 def test_bench_multi_rank_runs(ff, parallel):
     """bench.py under torchrun, 2 ranks, emulated on the one GPU (gloo rendezvous, both
     ranks time-sliced on GPU 0). Default (None) = tensor parallel over d_ffn (the north
     star's split) with the sequence-parallel residual; sp = the prompt's blocks split with
-    no collective; dp = one prompt per rank (BASELINE configs[4], weak scaling). The JSON
-    line must be well formed and name the split."""
+    no collective; dp = one prompt per rank (BASELINE configs[4], weak scaling); sharded =
+    the default split with the sequence-parallel predictor (each rank predicts its own
+    blocks, the selection bitmasks are all-gathered). The JSON line must be well formed
+    and name the split."""
     import json
     import os
     import socket
@@ -97,13 +99,17 @@ def test_bench_multi_rank_runs(ff, parallel):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={port}", "bench.py", "--gpus", "2",
            "--config", "1b", "--layers", "2", "--steps", "2", "--warmup", "3"]
-    if parallel is not None:
+    if parallel == "sharded":
+        cmd += ["--predictor", "sharded"]
+    elif parallel is not None:
         cmd += ["--parallel", parallel]
     r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=400)
     assert r.returncode == 0, r.stderr[-3000:]
     line = [l for l in r.stdout.splitlines() if l.startswith("{")][-1]
     d = json.loads(line)
-    want = {None: "tp2", "sp": "sp2", "dp": "dp2"}[parallel]
+    want = {None: "tp2", "sharded": "tp2", "sp": "sp2", "dp": "dp2"}[parallel]
+    if parallel == "sharded":
+        assert "sequence-parallel predictor" in d["collective"]
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == want
     assert d["scaling"] == ("weak" if parallel == "dp" else "strong")
     assert d["value"] > 0 and d["e2e"]["value"] > 0

@@ -50,7 +50,7 @@ def host_model():
     return out
 
 
-def run_emulated(ff, model, world, reduce_dtype, n_layers=L):
+def run_emulated(ff, model, world, reduce_dtype, n_layers=L, shard_predictor=False):
     from paper_2602_00397_b200.tp import SeqParallelTP, seq_rows
     dps = [ff.DevicePredictor.from_params(ff.PredictorParams(**p), "cuda") for _, p, _, _ in model]
     sps = []
@@ -60,7 +60,7 @@ def run_emulated(ff, model, world, reduce_dtype, n_layers=L):
                                  tp_size=world), dps[l], k)
                   for l, (w, _, c, k) in enumerate(model[:n_layers])]
         sps.append(SeqParallelTP(layers, T, D, r, world, "cuda", comm=None,
-                                 reduce_dtype=reduce_dtype))
+                                 reduce_dtype=reduce_dtype, shard_predictor=shard_predictor))
     x0 = torch.randn((T, D), generator=torch.Generator().manual_seed(9)).to(
         torch.bfloat16).float().cuda()
     h = [x0[slice(*seq_rows(T, r, world))].clone() for r in range(world)]
@@ -68,11 +68,16 @@ def run_emulated(ff, model, world, reduce_dtype, n_layers=L):
     for l in range(n_layers):
         for r in range(world):
             sps[r].norm(l, h[r])
+            sps[r].predict(l)                             # own blocks only (sharded)
         x_full = torch.cat([sp.x_shard for sp in sps])   # all-gather
         lg_full = torch.cat([sp.lg_shard for sp in sps])
+        if shard_predictor:
+            mask_full = torch.cat([sp.mask_shard for sp in sps])
         for sp in sps:
             sp.x_full.copy_(x_full)
             sp.lg_full.copy_(lg_full)
+            if shard_predictor:
+                sp.mask_full.copy_(mask_full)
             sp.ffn(l)
         total = sps[0].y_part.float().clone()            # reduce-scatter, rank order
         for sp in sps[1:]:
@@ -87,7 +92,8 @@ def run_emulated(ff, model, world, reduce_dtype, n_layers=L):
                 _, ir = ff.sparse_ffn_layer(x_full, packed, dp, k, logits_in=lg_full,
                                             return_indices=True)
                 idx.append(ir)
-            first = {"x": x_full.clone(), "lg": lg_full.clone(), "idx": idx}
+            first = {"x": x_full.clone(), "lg": lg_full.clone(), "idx": idx,
+                     "mask": mask_full.clone() if shard_predictor else None}
     for r, sp in enumerate(sps):
         sp.finish(h[r])
     torch.cuda.synchronize()
@@ -116,3 +122,45 @@ def test_seq_parallel_tp_matches_unsharded(ff, world, reduce):
     if reduce == "f32":  # the bf16 reduce's per-layer rounding moves later layers' inputs
         rel = float((hn - h1).double().norm() / h1.double().norm())
         assert rel <= 5e-3, rel
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_predictor_matches_replicated(ff, world):
+    """The sequence-parallel predictor (each rank predicts only its own T/N rows' blocks,
+    the selection bitmasks are all-gathered) gives every block the unsharded layer's
+    indices bit for bit, and the stack the same output as the replicated predictor."""
+    model = host_model()
+    h_rep, rep = run_emulated(ff, model, world, torch.float32)
+    h_sh, sh = run_emulated(ff, model, world, torch.float32, shard_predictor=True)
+    n_pred = T // 128 - 2
+    rows = ff.mask_indices(sh["mask"][1:1 + n_pred], F)  # blocks 1 .. n-2 are predicted
+    want = rep["idx"][0].cpu().numpy()
+    assert len(rows) == want.shape[0]
+    for b, row in enumerate(rows):
+        assert np.array_equal(row, want[b]), f"block {b + 1}: gathered mask != selection"
+    assert torch.equal(h_sh, h_rep), "sharded and replicated predictors differ"
+
+
+def test_predict_mask_and_mask_in_reproduce_the_layer(ff):
+    """One GPU: ``predict_mask`` over a block range equals the indices the layer selects
+    for those blocks, and ``sparse_ffn_layer(mask_in=...)`` (the selection given) is
+    bit-identical to the layer running its own predictor (tp_size 1 and a TP=2 shard)."""
+    w, pred, comp, k = host_model()[0]
+    dp = ff.DevicePredictor.from_params(ff.PredictorParams(**pred), "cuda")
+    x = torch.randn((T, D), generator=torch.Generator().manual_seed(3)).to(torch.bfloat16).cuda()
+    n_blk = T // 128
+    mask = torch.zeros((n_blk, ff.mask_words(F)), dtype=torch.int32, device="cuda")
+    ff.predict_mask(x, dp, k, blk_begin=1, blk_count=5, out=mask[1:6])
+    ff.predict_mask(x, dp, k, blk_begin=6, blk_count=n_blk - 7, out=mask[6:n_blk - 1])
+    for tp_size in (1, 2):
+        for rank in range(tp_size):
+            packed = ff.pack_layer(w["w_gate"], w["w_up"], w["w_down"], ff.CompensatorParams(**comp),
+                                   device="cuda", tp_rank=rank, tp_size=tp_size)
+            y_ref, idx = ff.sparse_ffn_layer(x, packed, dp, k, return_indices=True)
+            y_m = ff.sparse_ffn_layer(x, packed, dp, k, mask_in=mask)
+            assert torch.equal(y_m, y_ref), (tp_size, rank)
+    rows = ff.mask_indices(mask[1:n_blk - 1], F)
+    for b, row in enumerate(rows):
+        assert np.array_equal(row, idx[b].cpu().numpy()), b
+    with pytest.raises(ff.errors.ValidationError):
+        ff.sparse_ffn_layer(x, packed, dp, k, mask_in=mask[:, :3].contiguous())

@@ -158,9 +158,10 @@ def _sp_tp_model(d=512, f=1376, L=2, seed=31):
     return layers
 
 
-def _ffn_blocks(x, lw, pred, comp, k, nid=None, rank=0, world=1):
+def _ffn_blocks(x, lw, pred, comp, k, nid=None, rank=0, world=1, given=None):
     """The engine's FFN branch over all blocks of x (engine.py:254-310), on the neuron
-    shard `nid` (strided, rank of world) when given; returns (y, global index rows)."""
+    shard `nid` (strided, rank of world) when given; returns (y, global index rows).
+    `given` {block: global index row} replaces the predictor (a gathered selection)."""
     T = x.shape[0]
     n_blk = T // 128
     y = np.zeros_like(x)
@@ -177,8 +178,11 @@ def _ffn_blocks(x, lw, pred, comp, k, nid=None, rank=0, world=1):
         if j in (0, n_blk - 1):
             y[j * 128:(j + 1) * 128] = orc.dense_ffn(xb, gs, us, ds)
             continue
-        s = orc.predictor_forward(pred["query"], pred["w1"], pred["w2"], xb)
-        g = orc.topk_indices(s, k)
+        if given is not None:
+            g = given[j]
+        else:
+            s = orc.predictor_forward(pred["query"], pred["w1"], pred["w2"], xb)
+            g = orc.topk_indices(s, k)
         sel[j] = g
         loc = g if nid is None else g[g % world == rank] // world
         yb = orc.sparse_ffn_forward(xb, gs, us, ds, loc) if loc.size else 0.0
@@ -187,10 +191,20 @@ def _ffn_blocks(x, lw, pred, comp, k, nid=None, rank=0, world=1):
     return y, sel
 
 
-def _sp_tp_worker(rank, world, port, out):
+def _pack_mask(rows, f):
+    """Selection bitmasks (layer.predict_mask's format) of index rows, int32 words."""
+    m = np.zeros((len(rows), (f + 31) // 32), np.uint32)
+    for i, g in enumerate(rows):
+        np.bitwise_or.at(m[i], g >> 5, (np.uint32(1) << (g & 31).astype(np.uint32)))
+    return m.view(np.int32)
+
+
+def _sp_tp_worker(rank, world, port, out, sharded=False):
     """SeqParallelTP with gloo collectives and the oracle in place of the kernels: each
     rank owns T/N residual rows, normalises them, all-gathers x and the logits, runs the
-    FFN branch on its strided d_ffn shard, reduce-scatters the partial y."""
+    FFN branch on its strided d_ffn shard, reduce-scatters the partial y.  `sharded`:
+    the sequence-parallel predictor -- each rank predicts its own blocks, the ranks
+    all-gather the selection bitmasks instead of the logits."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -202,7 +216,7 @@ def _sp_tp_worker(rank, world, port, out):
         h0 = orc.bf16_round(np.random.default_rng(5).standard_normal((T, d)).astype(np.float32))
         r0, r1 = seq_rows(T, rank, world)
         nid = shard_neurons(f, rank, world)
-        log = {"sel_ok": True, "lg_ok": True}
+        log = {"sel_ok": True, "lg_ok": True, "predicted": 0}
 
         def norm_fn(l, h_shard, add):
             if add is not None:
@@ -212,18 +226,35 @@ def _sp_tp_worker(rank, world, port, out):
             q = model[l][1]["query"]
             sp.lg_shard.copy_(torch.from_numpy(orc.mm(q, x.T)[0] / np.float32(np.sqrt(d))))
 
-        def ffn_fn(l, x_full, lg_full, y_part):
+        def predict_fn(l, lo, hi):  # this rank's own blocks -> bitmask rows
+            _, pred, _, k = model[l]
+            x = sp.x_shard.numpy()
+            rows = [orc.topk_indices(orc.predictor_forward(pred["query"], pred["w1"], pred["w2"],
+                                                           x[b * 128:(b + 1) * 128]), k)
+                    for b in range(lo, hi)]
+            sp.mask_shard[lo:hi].copy_(torch.from_numpy(_pack_mask(rows, f)))
+            log["predicted"] += hi - lo
+
+        def ffn_fn(l, x_full, sel_full, y_part):
             lw, pred, comp, k = model[l]
             x = x_full.numpy()
-            want_lg = orc.mm(pred["query"], x.T)[0] / np.float32(np.sqrt(d))
-            log["lg_ok"] &= bool(np.array_equal(lg_full.numpy(), want_lg))
-            y, sel = _ffn_blocks(x, lw, pred, comp, k, nid, rank, world)
-            _, sel_full = _ffn_blocks(x, lw, pred, comp, k)
-            log["sel_ok"] &= all(np.array_equal(sel[j], sel_full[j]) for j in sel)
+            _, want_sel = _ffn_blocks(x, lw, pred, comp, k)
+            given = None
+            if sharded:  # the gathered bitmasks are every block's global selection
+                m = sel_full.numpy().view(np.uint32)
+                bits = np.unpackbits(m.view(np.uint8), axis=1, bitorder="little")[:, :f]
+                given = {j: np.flatnonzero(bits[j]) for j in want_sel}
+            else:
+                want_lg = orc.mm(pred["query"], x.T)[0] / np.float32(np.sqrt(d))
+                log["lg_ok"] &= bool(np.array_equal(sel_full.numpy(), want_lg))
+            y, sel = _ffn_blocks(x, lw, pred, comp, k, nid, rank, world, given=given)
+            log["sel_ok"] &= all(np.array_equal(sel[j], want_sel[j]) for j in want_sel)
             y_part.copy_(torch.from_numpy(y))
 
-        sp = SeqParallelTP([None] * len(model), T, d, rank, world, "cpu", comm=TorchComm(),
-                           norm_fn=norm_fn, ffn_fn=ffn_fn, x_dtype=torch.float32)
+        sp = SeqParallelTP([(None, None, k) for _, _, _, k in model], T, d, rank, world, "cpu",
+                           comm=TorchComm(), norm_fn=norm_fn, ffn_fn=ffn_fn,
+                           predict_fn=predict_fn, x_dtype=torch.float32,
+                           shard_predictor=sharded, f=f)
         h = torch.from_numpy(h0[r0:r1].copy())
         sp.stack(h)
         parts = [None] * world
@@ -235,15 +266,21 @@ def _sp_tp_worker(rank, world, port, out):
 
 
 @pytest.mark.timeout(600)
-def test_sp_tp2_reduce_scatter_all_gather_matches_reference():
+@pytest.mark.parametrize("sharded", [False, True], ids=["replicated_predictor",
+                                                       "sharded_predictor"])
+def test_sp_tp2_reduce_scatter_all_gather_matches_reference(sharded):
     """World 2: the sequence-parallel TP stack (reduce-scatter / all-gather around the
     FFN branch, engine.py:263-308 split over d_ffn and over the residual rows) equals the
-    unsharded reference chain h <- h + FFN(rmsnorm(h)) over two layers."""
+    unsharded reference chain h <- h + FFN(rmsnorm(h)) over two layers.  Sharded: each
+    rank predicts only its own blocks (4 of the 8; the dense first / last excluded) and
+    the gathered bitmasks equal every block's global selection."""
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_sp_tp_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    mp.spawn(_sp_tp_worker, args=(2, _free_port(), out, sharded), nprocs=2, join=True)
     parts = sorted(out["parts"], key=lambda p: p[0])
     assert all(p[2]["sel_ok"] and p[2]["lg_ok"] for p in parts)
+    # layers x own predicted blocks: rank 0 skips block 0, rank 1 block 7
+    assert [p[2]["predicted"] for p in parts] == ([2 * 3, 2 * 3] if sharded else [0, 0])
     h_tp = np.concatenate([p[1] for p in parts])
     d, T = 512, 1024
     h = orc.bf16_round(np.random.default_rng(5).standard_normal((T, d)).astype(np.float32))
