@@ -21,6 +21,9 @@ namespace ffwd {
 
 namespace {
 
+#ifndef FFWD_PLAN_BESIDE_TOPK
+#define FFWD_PLAN_BESIDE_TOPK 1
+#endif
 constexpr int kPlanThreads = 512;
 constexpr int kMaxBlocks = 4096;
 constexpr int kUpBN = 256;  // rows per compensator up-projection tile
@@ -42,7 +45,12 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
   __shared__ short s_ngu[kMaxBlocks];   // of which gate/up tiles
   __shared__ int s_gbase[kMaxBlocks + 1];
   __shared__ int s_hcols;
-  pdl_wait();
+  // Without per-block counts (no tensor parallelism) the plan does not read the top-k's
+  // output, so it runs beside the top-k kernel and waits for it only before exiting: the
+  // up projection's wait on the plan then still covers the indices.  Every earlier kernel
+  // of the layer waited for its predecessor before releasing its dependents, so the
+  // previous layer's GEMMs (which read these tables) are complete when this one starts.
+  if (a.counts || !FFWD_PLAN_BESIDE_TOPK) pdl_wait();
   pdl_trigger();
   const int tid = threadIdx.x;
   const int rc64 = rup(a.rc_local, 64);
@@ -172,6 +180,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
     pc->n_down = total_down;
     pc->hcols = s_hcols;
   }
+  if (!a.counts && FFWD_PLAN_BESIDE_TOPK) pdl_wait();
 }
 
 }  // namespace
