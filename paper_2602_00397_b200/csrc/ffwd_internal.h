@@ -146,32 +146,6 @@ struct GemmArgs {
                      // (the overlapped TP completion consumes blocks as they finish)
 };
 
-// A pair tile of the CTA-pair down projection (down_pair.cu): blocks b0 (CTA 0) and b1
-// (CTA 1), whose index lists (row `row` of idx, b0's) share their first 64 nk neurons;
-// output columns [n0, n0 + 256).  b0 < 0 = empty slot.
-struct PairTile {
-  int b0, b1, n0, nk;
-  int row, pad0, pad1, pad2;
-};
-
-struct PairArgs {
-  const void* h;        // bf16 [n_blk*128 x hcols]
-  int hcols;
-  const void* wd;       // bf16 [wd_rows x d]
-  int wd_rows;
-  int T, d, n_blk;
-  float* y;             // f32 [T x d]: y = residual + the pair part
-  const float* residual;  // nullable
-  const int32_t* idx;
-  int ld_idx;
-  const PairTile* tiles;
-  int n_tiles;
-  int* blk_done;        // nullable: wait for the up projection per block
-  const BlockMeta* meta;
-  int num_sms;
-};
-cudaError_t launch_down_pair(const PairArgs& a, cudaStream_t s);
-
 cudaError_t launch_up_proj(const GemmArgs& a, cudaStream_t s);
 bool up_proj_paired();    // the up projection runs as CTA pairs (tile table in pairs)
 bool down_proj_paired();  // the down projection runs as CTA pairs
