@@ -42,6 +42,13 @@
 #ifdef FFWD_K3_A_LDGSTS
 #define FFWD_A_LDGSTS
 #endif
+// Dynamic tile claiming (FFWD_K3_DYN, default on): gemm_sm100.cuh TileQueue.
+#ifndef FFWD_K3_DYN
+#define FFWD_K3_DYN 1
+#endif
+#if FFWD_K3_DYN
+#define FFWD_DYN_TILES
+#endif
 #include "gemm_sm100.cuh"
 #include "launch.cuh"
 
@@ -114,6 +121,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_trigger();
   const uint32_t tmem = sm.bar->tmem_base;
   const int n_tiles = a.counts->n_down;
+  // every role walks the same tile sequence: claimed dynamically (TileQueue) or strided
+  // (producer warp 0 claims; the other roles follow its sequence)
+  TileCursor cur;
+  int* const claim_ctr = const_cast<int*>(&a.counts->next_down);
+  auto fetch = [&](bool warp_wide) {
+    return warp == 0 ? cur.claim(&sm.bar->q, claim_ctr, n_tiles) : cur.next(&sm.bar->q, warp_wide);
+  };
+  auto first_tile = [&](bool warp_wide) {
+    return kDyn ? fetch(warp_wide) : static_cast<int>(blockIdx.x);
+  };
+  auto next_tile = [&](int t, bool warp_wide) {
+    return kDyn ? fetch(warp_wide) : t + static_cast<int>(gridDim.x);
+  };
+  auto more = [&](int t) { return kDyn ? t >= 0 : t < n_tiles; };
 
   if (warp < kProducerWarps) {
     // ---------------- producers: warp w gathers K rows [Q w, Q w + Q) of every stage
@@ -125,7 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t pol_w = pol(FFWD_K3_W_POLICY);
     int* rows = sm.bar->rows[warp];
     uint32_t stage = 0, phase = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (int t = first_tile(true); more(t); t = next_tile(t, true)) {
       const Tile tl = a.down_tiles[t];
       if (tl.b < 0) continue;
       const BlockMeta m = a.meta[tl.b];
@@ -212,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // at r * 128 + ((c ^ (r & 7)) * 16))
     uint32_t sa = 0, pa = 0;
     const __nv_bfloat16* H = static_cast<const __nv_bfloat16*>(a.h);
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (int t = first_tile(true); more(t); t = next_tile(t, true)) {
       const Tile tl = a.down_tiles[t];
       if (tl.b < 0) continue;
       const int nk = a.meta[tl.b].ktot / BK;
@@ -244,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_h = FFWD_K3_H_POLICY == 2 ? policy_evict_last()
                                                    : policy_evict_normal();
       uint32_t sa = 0, pa = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int t = first_tile(false); more(t); t = next_tile(t, false)) {
         const Tile tl = a.down_tiles[t];
         if (tl.b < 0) continue;
         const int nk = a.meta[tl.b].ktot / BK;
@@ -276,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0;
       [[maybe_unused]] uint32_t sa = 0, pa = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int t = first_tile(false); more(t); t = next_tile(t, false)) {
         const Tile tl = a.down_tiles[t];
         if (tl.b < 0) continue;
         const BlockMeta m = a.meta[tl.b];
@@ -311,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - kEpiWarp0;
     const int row = ew * 32 + static_cast<int>(lane);
     uint32_t acc = 0, acc_phase = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (int t = first_tile(true); more(t); t = next_tile(t, true)) {
       const Tile tl = a.down_tiles[t];
       if (tl.b < 0) continue;
       const BlockMeta m = a.meta[tl.b];

@@ -33,10 +33,10 @@ struct Tile {
 };
 
 struct PlanCounts {
-  int n_up;    // entries in the up-projection tile table
-  int n_down;  // entries in the down-projection tile table
-  int hcols;   // H row stride actually used (<= the allocated stride)
-  int pad;
+  int n_up;       // entries in the up-projection tile table
+  int n_down;     // entries in the down-projection tile table
+  int hcols;      // H row stride actually used (<= the allocated stride)
+  int next_down;  // dynamic tile claiming of the down projection (zeroed by the plan)
 };
 
 // ------------------------------------------------------------------ K1

@@ -59,6 +59,14 @@ constexpr int kProducerWarps = FFWD_PRODUCER_WARPS;  // TMA gather4 issue rate s
 constexpr int kEpiWarp0 = kProducerWarps;            // multiple of 4: warp % 4 = TMEM lane quadrant
 constexpr int kMmaWarp = kProducerWarps + 4;
 constexpr int kAWarp = kProducerWarps + 5;  // A loader (split rings only)
+// Dynamic tile claiming (FFWD_DYN_TILES, per kernel TU; TileQueue below)
+#ifdef FFWD_DYN_TILES
+constexpr bool kDyn = true;
+#else
+constexpr bool kDyn = false;
+#endif
+// warps reading the tile queue: all roles but producer warp 0, which claims
+constexpr int kTileConsumers = kProducerWarps + 4 + (kSplit ? 1 : 0);
 constexpr int kThreads = (kProducerWarps + 5 + (kSplit ? 1 : 0)) * 32;
 static_assert(kProducerWarps % 4 == 0 && 64 % kProducerWarps == 0, "producer split");
 constexpr uint32_t kTmemCols = 512;
@@ -84,6 +92,64 @@ __host__ __device__ constexpr int round_up(int v, int m) { return (v + m - 1) / 
 #endif
 constexpr int kGatherRows = FFWD_GATHER_ROWS;
 
+// Dynamic tile claiming: producer warp 0 claims the CTA's next tile from a global counter
+// (atomicAdd, table order) when it is about to start it, and hands the id to the CTA's
+// other roles through a small shared-memory queue, so every role walks the same
+// sequence.  A CTA thus takes a tile exactly when its gathers are ready for one: the long
+// tiles (dense blocks) and the last wave no longer set the kernel's end as with static
+// striding.  Each tile's arithmetic is unchanged (results are bit-identical).
+constexpr int kTQ = 4;
+struct TileQueue {
+  uint64_t full[kTQ];
+  uint64_t empty[kTQ];  // one arrival per consuming warp
+  int tile[kTQ];
+};
+
+__device__ __forceinline__ void tq_init(TileQueue* q, uint32_t consumers) {
+  for (int i = 0; i < kTQ; ++i) {
+    mbar_init(&q->full[i], 1);
+    mbar_init(&q->empty[i], consumers);
+  }
+}
+
+struct TileCursor {
+  uint32_t i = 0, ph = 0;
+  // Consumers: the next tile id (-1 = no more).  `warp_wide`: every lane of the warp
+  // calls it (lane 0 releases the slot after the warp read it); else a single thread.
+  __device__ __forceinline__ int next(TileQueue* q, bool warp_wide) {
+    mbar_wait(&q->full[i], ph);
+    const int t = q->tile[i];
+    if (warp_wide) {
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&q->empty[i]);
+    } else {
+      mbar_arrive(&q->empty[i]);
+    }
+    advance();
+    return t;
+  }
+  // The claiming warp (all lanes): claims the next tile, posts it, returns it.
+  __device__ __forceinline__ int claim(TileQueue* q, int* counter, int n_tiles) {
+    int t = 0;
+    if ((threadIdx.x & 31) == 0) {
+      mbar_wait(&q->empty[i], ph ^ 1);
+      t = atomicAdd(counter, 1);
+      if (t >= n_tiles) t = -1;
+      q->tile[i] = t;
+      mbar_arrive(&q->full[i]);
+    }
+    t = __shfl_sync(0xffffffffu, t, 0);
+    advance();
+    return t;
+  }
+  __device__ __forceinline__ void advance() {
+    if (++i == kTQ) {
+      i = 0;
+      ph ^= 1;
+    }
+  }
+};
+
 struct Barriers {
   uint64_t full[kStagesB];   // B (and, unsplit, A) landed
   uint64_t empty[kStagesB];
@@ -93,6 +159,7 @@ struct Barriers {
   uint64_t tempty[2];
   uint32_t tmem_base;
   uint32_t pad;
+  TileQueue q;  // dynamic tile claiming only
   alignas(16) int rows[kProducerWarps][kGatherRows / kProducerWarps];  // gather row ids (int4)
 };
 
@@ -133,6 +200,7 @@ __device__ __forceinline__ void prologue(Smem<kBBytes>& sm, int warp) {
       mbar_init(&sm.bar->tfull[i], 1);
       mbar_init(&sm.bar->tempty[i], 128);
     }
+    if constexpr (kDyn) tq_init(&sm.bar->q, kTileConsumers);
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc<kTmemCols>(&sm.bar->tmem_base);
