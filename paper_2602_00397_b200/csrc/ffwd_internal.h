@@ -37,6 +37,8 @@ struct PlanCounts {
   int n_down;     // entries in the down-projection tile table
   int hcols;      // H row stride actually used (<= the allocated stride)
   int next_down;  // dynamic tile claiming of the down projection (zeroed by the plan)
+  int next_up;    // ... of the up projection (in CTA-pair units when paired)
+  int pad[3];
 };
 
 // ------------------------------------------------------------------ K1

@@ -112,6 +112,32 @@ __device__ __forceinline__ void tq_init(TileQueue* q, uint32_t consumers) {
   }
 }
 
+// Cluster-scope acquire wait (the peer CTA posted the slot with a remote release-arrive).
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void st_shared_remote(int* p, uint32_t rank, int v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(remote), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+
 struct TileCursor {
   uint32_t i = 0, ph = 0;
   // Consumers: the next tile id (-1 = no more).  `warp_wide`: every lane of the warp
@@ -141,6 +167,36 @@ struct TileCursor {
     t = __shfl_sync(0xffffffffu, t, 0);
     advance();
     return t;
+  }
+  // CTA pairs (the two CTAs of a cluster run table slots 2p and 2p + 1 together): rank 0's
+  // producer warp 0 claims a pair index p and posts it into both CTAs' queues; every
+  // consumer of either CTA releases the slot on rank 0's queue (its empty barrier counts
+  // both CTAs' consumers).  Returns this CTA's slot 2p + rank (-1 = no more).
+  __device__ __forceinline__ int claim_pair(TileQueue* q, int* counter, int n_tiles) {
+    int p = 0;
+    if ((threadIdx.x & 31) == 0) {
+      mbar_wait_cluster(&q->empty[i], ph ^ 1);
+      p = atomicAdd(counter, 1);
+      if (2 * p >= n_tiles) p = -1;
+      q->tile[i] = p;
+      st_shared_remote(&q->tile[i], 1, p);
+      mbar_arrive(&q->full[i]);
+      mbar_arrive_remote(&q->full[i], 1);
+    }
+    p = __shfl_sync(0xffffffffu, p, 0);
+    advance();
+    return p < 0 ? -1 : 2 * p;
+  }
+  __device__ __forceinline__ int next_pair(TileQueue* q, bool warp_wide, uint32_t rank) {
+    mbar_wait_cluster(&q->full[i], ph);
+    const int p = q->tile[i];
+    if (warp_wide) __syncwarp();
+    if (!warp_wide || (threadIdx.x & 31) == 0) {
+      if (rank == 0) mbar_arrive(&q->empty[i]);
+      else mbar_arrive_remote(&q->empty[i], 0);
+    }
+    advance();
+    return p < 0 ? -1 : 2 * p + static_cast<int>(rank);
   }
   __device__ __forceinline__ void advance() {
     if (++i == kTQ) {
@@ -200,7 +256,8 @@ __device__ __forceinline__ void prologue(Smem<kBBytes>& sm, int warp) {
       mbar_init(&sm.bar->tfull[i], 1);
       mbar_init(&sm.bar->tempty[i], 128);
     }
-    if constexpr (kDyn) tq_init(&sm.bar->q, kTileConsumers);
+    // pairs: rank 0's empty barriers count both CTAs' consumers (the peer's warp 0 too)
+    if constexpr (kDyn) tq_init(&sm.bar->q, kPairA ? 2 * kTileConsumers + 1 : kTileConsumers);
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc<kTmemCols>(&sm.bar->tmem_base);

@@ -180,6 +180,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
     pc->n_down = total_down;
     pc->hcols = s_hcols;
     pc->next_down = 0;
+    pc->next_up = 0;
   }
   if (!a.counts && FFWD_PLAN_BESIDE_TOPK) pdl_wait();
 }

@@ -32,6 +32,13 @@
 #define FFWD_STAGES_B 5
 #endif
 #endif
+// Dynamic tile claiming (FFWD_K2_DYN, default on; CTA pairs claim slot pairs together)
+#ifndef FFWD_K2_DYN
+#define FFWD_K2_DYN 1
+#endif
+#if FFWD_K2_DYN
+#define FFWD_DYN_TILES
+#endif
 #include "gemm_sm100.cuh"
 #include "launch.cuh"
 
@@ -75,6 +82,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   pdl_trigger();
   const uint32_t tmem = sm.bar->tmem_base;
   const int n_tiles = a.counts->n_up;
+  // every role walks the same tile sequence: claimed dynamically by producer warp 0 (of
+  // rank 0 for a CTA pair) or strided
+  TileCursor cur;
+  int* const claim_ctr = const_cast<int*>(&a.counts->next_up);
+  const uint32_t crank = kPairA ? cluster_ctarank() : 0;
+  auto fetch = [&](bool warp_wide) -> int {
+    if constexpr (kPairA) {
+      return (warp == 0 && crank == 0) ? cur.claim_pair(&sm.bar->q, claim_ctr, n_tiles)
+                                       : cur.next_pair(&sm.bar->q, warp_wide, crank);
+    } else {
+      return warp == 0 ? cur.claim(&sm.bar->q, claim_ctr, n_tiles)
+                       : cur.next(&sm.bar->q, warp_wide);
+    }
+  };
+  auto first_tile = [&](bool warp_wide) {
+    return kDyn ? fetch(warp_wide) : static_cast<int>(blockIdx.x);
+  };
+  auto next_tile = [&](int t, bool warp_wide) {
+    return kDyn ? fetch(warp_wide) : t + static_cast<int>(gridDim.x);
+  };
+  auto more = [&](int t) { return kDyn ? t >= 0 : t < n_tiles; };
   const int nk = a.d / BK;
 
   if (warp < kProducerWarps) {
@@ -88,7 +116,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                            : FFWD_K2_W_POLICY == 1 ? policy_evict_first() : policy_evict_normal();
     int* rows = sm.bar->rows[warp];
     uint32_t stage = 0, phase = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (int t = first_tile(true); more(t); t = next_tile(t, true)) {
       const Tile tl = a.up_tiles[t];
       if (tl.b < 0) continue;
       const BlockMeta m = a.meta[tl.b];
@@ -158,7 +186,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_x = FFWD_K2_X_POLICY == 2 ? policy_evict_last()
                              : FFWD_K2_X_POLICY == 1 ? policy_evict_first() : policy_evict_normal();
       uint32_t sa = 0, pa = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int t = first_tile(false); more(t); t = next_tile(t, false)) {
         const Tile tl = a.up_tiles[t];
         if (tl.b < 0) continue;
         const int tok0 = a.meta[tl.b].tok0;
@@ -186,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       pr.t0 = clock64();
 #endif
       uint32_t stage = 0, phase = 0, acc = 0, acc_phase = 0, sa = 0, pa = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int t = first_tile(false); more(t); t = next_tile(t, false)) {
         const Tile tl = a.up_tiles[t];
         if (tl.b < 0) continue;
 #ifdef FFWD_PROBE
@@ -219,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - kEpiWarp0;
     const int row = ew * 32 + static_cast<int>(lane);
     uint32_t acc = 0, acc_phase = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (int t = first_tile(true); more(t); t = next_tile(t, true)) {
       const Tile tl = a.up_tiles[t];
       if (tl.b < 0) continue;
       const BlockMeta m = a.meta[tl.b];
