@@ -5,6 +5,8 @@ kernel at parity sizes, checked against the oracle so a silent corruption also f
          top-k, plan, K2 (CTA pairs, multicast), K3 (per-block K2->K3 counters, PDL)
   edge   short / single-token blocks, k = 1, k = f - 1, ragged compensator, 64-col tiles
   norm   the FFN-input RMSNorm with fused logits and residual add
+  mask   the sequence-parallel predictor's halves: predict_mask over a block range (top-k
+         with bitmask output) and the masked layer at TP=2 (bitmask-to-list kernel)
   tp1    the fused TP completion kernel with one rank (the sanitizer serialises kernel
          launches, so two emulated ranks that wait on each other cannot both run under it;
          the two-rank flag protocol is covered by tests/test_gpu_tp_fused.py)
@@ -73,6 +75,32 @@ def case_norm():
     print("norm: ok")
 
 
+def case_mask():
+    d, f, T = 512, 1376, 1024
+    k = ff.budget_to_k(0.5, f)
+    rng = np.random.default_rng(77)
+    lw = orc.random_layer(rng, d, f, 0.02)
+    for key in ("w_gate", "w_up", "w_down"):
+        lw[key] = orc.bf16_round(lw[key])
+    pred = orc.init_predictor(np.random.default_rng([77, 1]), d, f)
+    comp = {n: orc.bf16_round(v) for n, v in
+            orc.init_compensator(np.random.default_rng([77, 2]), d).items()}
+    x = torch.from_numpy(orc.bf16_round(rng.standard_normal((T, d)).astype(np.float32)))
+    x = x.to("cuda", torch.bfloat16)
+    dp = ff.DevicePredictor.from_params(ff.PredictorParams(**pred), "cuda")
+    n_blk = T // 128
+    mask = torch.zeros((n_blk, ff.mask_words(f)), dtype=torch.int32, device="cuda")
+    ff.predict_mask(x, dp, k, blk_begin=1, blk_count=n_blk - 2, out=mask[1:n_blk - 1])
+    for rank in range(2):
+        packed = ff.pack_layer(lw["w_gate"], lw["w_up"], lw["w_down"], ff.CompensatorParams(**comp),
+                               device="cuda", tp_rank=rank, tp_size=2)
+        y_ref = ff.sparse_ffn_layer(x, packed, dp, k)
+        y_m = ff.sparse_ffn_layer(x, packed, dp, k, mask_in=mask)
+        torch.cuda.synchronize()
+        assert torch.equal(y_m, y_ref), rank
+    print("mask (predict_mask + masked TP=2 layer): ok")
+
+
 def case_tp1():
     from paper_2602_00397_b200.tp import allreduce_residual_fused
     n, T, d = 1, 300, 256
@@ -91,6 +119,6 @@ def case_tp1():
 
 
 if __name__ == "__main__":
-    cases = sys.argv[1:] or ["cfg1", "edge", "norm", "tp1"]
+    cases = sys.argv[1:] or ["cfg1", "edge", "norm", "mask", "tp1"]
     for c in cases:
         globals()[f"case_{c}"]()
