@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // every role walks the same tile sequence: claimed dynamically (TileQueue) or strided
   // (producer warp 0 claims; the other roles follow its sequence)
   TileCursor cur;
-  int* const claim_ctr = const_cast<int*>(&a.counts->next_down);
+  int* const claim_ctr = &a.counts->next_down;
   auto fetch = [&](bool warp_wide) {
     return warp == 0 ? cur.claim(&sm.bar->q, claim_ctr, n_tiles) : cur.next(&sm.bar->q, warp_wide);
   };

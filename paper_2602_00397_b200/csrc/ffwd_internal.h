@@ -140,7 +140,7 @@ struct GemmArgs {
   int up_cap;
   const Tile* down_tiles;
   int down_cap;
-  const PlanCounts* counts;
+  PlanCounts* counts;   // tile counts (read) and the dynamic-claim counters (atomics)
   int num_sms;
   int bn_down;
   int* blk_done;  // nullable: block-granular K2 -> K3 dependency (per-block done tiles)

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // every role walks the same tile sequence: claimed dynamically by producer warp 0 (of
   // rank 0 for a CTA pair) or strided
   TileCursor cur;
-  int* const claim_ctr = const_cast<int*>(&a.counts->next_up);
+  int* const claim_ctr = &a.counts->next_up;
   const uint32_t crank = kPairA ? cluster_ctarank() : 0;
   auto fetch = [&](bool warp_wide) -> int {
     if constexpr (kPairA) {
