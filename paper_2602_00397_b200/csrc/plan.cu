@@ -21,6 +21,9 @@ namespace ffwd {
 
 namespace {
 
+#ifndef FFWD_MERGE_DENSE
+#define FFWD_MERGE_DENSE 1
+#endif
 #ifndef FFWD_PLAN_BESIDE_TOPK
 #define FFWD_PLAN_BESIDE_TOPK 1
 #endif
@@ -45,6 +48,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
   __shared__ short s_ngu[kMaxBlocks];   // of which gate/up tiles
   __shared__ int s_gbase[kMaxBlocks + 1];
   __shared__ int s_hcols;
+  __shared__ int s_q, s_dp, s_dn;  // merged dense group: rows, dense pairs, dense tiles
   // Without per-block counts (no tensor parallelism) the plan does not read the top-k's
   // output, so it runs beside the top-k kernel and waits for it only before exiting: the
   // up projection's wait on the plan then still covers the indices.  Every earlier kernel
@@ -87,14 +91,44 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
   }
   __syncthreads();
 
-  // groups never straddle the dense / predicted boundary
+  // Up-projection raster groups.  Predicted blocks: groups of up_group blocks,
+  // tile-index-major.  The dense blocks (first / last) join the first predicted group
+  // (FFWD_MERGE_DENSE, CTA pairs only): their tile pairs are spread over that group's
+  // tile-pair rows in neuron order, so a dense tile reads the W_gu rows the predicted
+  // tiles of the same row read (at 50% keep, dense tiles 2p, 2p+1 cover the neurons of
+  // predicted tile p) -- one sweep of the weights for both instead of a separate dense
+  // group that reads all of W_gu once more.  Otherwise the dense blocks form their own
+  // groups (groups never straddle the dense / predicted boundary).
   const int n_dense = a.n_blk - a.sparse_count;
-  const int g_dense = (n_dense + a.up_group - 1) / a.up_group;
-  const int g_total = g_dense + (a.sparse_count + a.up_group - 1) / a.up_group;
+  const bool merge = FFWD_MERGE_DENSE && a.pair_up && n_dense > 0 && a.sparse_count > 0;
+  const int g_dense = merge ? 0 : (n_dense + a.up_group - 1) / a.up_group;
+  const int sz0 = min(a.up_group, a.sparse_count);  // predicted blocks of the merged group
+  const int g_total = merge ? 1 + (a.sparse_count - sz0 + a.up_group - 1) / a.up_group
+                            : g_dense + (a.sparse_count + a.up_group - 1) / a.up_group;
+  // order range of group g (the merged group 0 spans the dense blocks and sz0 predicted)
+  auto group_range = [&](int g, int& o0, int& o1) {
+    if (merge) {
+      o0 = g == 0 ? 0 : n_dense + sz0 + (g - 1) * a.up_group;
+      o1 = g == 0 ? n_dense + sz0 : min(a.n_blk, o0 + a.up_group);
+    } else {
+      o0 = g < g_dense ? g * a.up_group : n_dense + (g - g_dense) * a.up_group;
+      o1 = min(g < g_dense ? n_dense : a.n_blk, o0 + a.up_group);
+    }
+  };
   // per-group slot counts (max tiles in the group x group size)
   for (int g = tid; g < g_total; g += kPlanThreads) {
-    const int o0 = g < g_dense ? g * a.up_group : n_dense + (g - g_dense) * a.up_group;
-    const int o1 = min(g < g_dense ? n_dense : a.n_blk, o0 + a.up_group);
+    int o0, o1;
+    group_range(g, o0, o1);
+    if (merge && g == 0) {
+      int mxp = 0, dn = 0;
+      for (int o = n_dense; o < o1; ++o) mxp = max(mxp, static_cast<int>(s_nup[o]));
+      for (int o = 0; o < n_dense; ++o) dn = max(dn, static_cast<int>(s_nup[o]));
+      s_q = max(1, rup(mxp, 2) / 2);  // tile-pair rows of the group
+      s_dp = (dn + 1) / 2;            // tile pairs per dense block
+      s_dn = dn;
+      s_gbase[1] = 2 * sz0 * s_q + 2 * n_dense * s_dp;
+      continue;
+    }
     int mx = 0;
     for (int o = o0; o < o1; ++o) mx = max(mx, static_cast<int>(s_nup[o]));
     if (a.pair_up) mx = rup(mx, 2);  // paired up-projection: whole (i, i+1) tile pairs
@@ -114,16 +148,41 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
       const int mid = (lo + hi + 1) >> 1;
       if (s_gbase[mid] <= slot) lo = mid; else hi = mid - 1;
     }
-    const int o0 = lo < g_dense ? lo * a.up_group : n_dense + (lo - g_dense) * a.up_group;
-    const int o1 = min(lo < g_dense ? n_dense : a.n_blk, o0 + a.up_group);
-    const int sz = o1 - o0;
+    int o0, o1;
+    group_range(lo, o0, o1);
     const int rel = slot - s_gbase[lo];
-    const int mx = (s_gbase[lo + 1] - s_gbase[lo]) / sz;  // tiles per block in this group
     int i, o;
-    if (a.pair_up) {
+    if (merge && lo == 0) {
+      // row pair q holds predicted tiles (2q, 2q+1) of each of the sz0 predicted blocks,
+      // then the dense tile pairs p in [ceil(q Dp / Q), ceil((q+1) Dp / Q)) of each dense
+      // block; row q starts at 2 q sz0 + 2 n_dense ceil(q Dp / Q)
+      const int Q = s_q, Dp = s_dp;
+      auto pfirst = [&](int q) { return (q * Dp + Q - 1) / Q; };
+      auto base = [&](int q) { return 2 * q * sz0 + 2 * n_dense * pfirst(q); };
+      int ql = 0, qh = Q - 1;
+      while (ql < qh) {
+        const int mid = (ql + qh + 1) >> 1;
+        if (base(mid) <= rel) ql = mid; else qh = mid - 1;
+      }
+      const int q = ql, r2 = rel - base(q);
+      if (r2 < 2 * sz0) {
+        const int h = r2 & 1;
+        o = n_dense + (r2 >> 1);
+        i = 2 * q + h;
+        if (h == 1 && i == s_nup[o]) i -= 1;
+      } else {
+        const int r3 = r2 - 2 * sz0, h = r3 & 1, c = pfirst(q + 1) - pfirst(q);
+        const int dp = r3 >> 1;
+        o = dp / c;                       // dense block (order)
+        i = 2 * (pfirst(q) + dp % c) + h;
+        if (i >= s_dn) i = s_dn - 1;      // odd tile count: repeat the last tile
+      }
+    } else if (a.pair_up) {
       // consecutive slots (2m, 2m + 1) = neuron tiles (2 i2, 2 i2 + 1) of ONE block: the
       // CTA pair running them shares the block's X tile by TMA multicast.  An odd tile
       // count repeats the block's last tile in the second slot (identical H writes).
+      const int sz = o1 - o0;
+      const int mx = (s_gbase[lo + 1] - s_gbase[lo]) / sz;  // tiles per block in this group
       const int pi = rel >> 1, h = rel & 1;
       int i2 = pi / sz;
       o = o0 + pi % sz;
@@ -131,6 +190,8 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a, BlockMet
       i = 2 * i2 + h;
       if (h == 1 && i == s_nup[o]) i -= 1;
     } else {
+      const int sz = o1 - o0;
+      const int mx = (s_gbase[lo + 1] - s_gbase[lo]) / sz;
       i = rel / sz;
       o = o0 + rel % sz;
       // serpentine: odd groups sweep the neuron tiles downwards, so the weight rows the
