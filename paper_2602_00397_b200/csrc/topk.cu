@@ -161,17 +161,24 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
   const uint32_t thr = prefix;    // key of the k-th largest score
   const int need_eq = remaining;  // how many keys == thr to keep (lowest index first)
 
-  // -- compaction in index order: contiguous chunk per thread
+  // -- compaction in index order: contiguous chunk per thread.  One pass counts the keys
+  // above the threshold and the ties; the ties are taken lowest index first.
   const bool tp1 = tp_size == 1;
   const int per = (f + kTopkThreads - 1) / kTopkThreads;
   const int lo = min(f, tid * per), hi = min(f, lo + per);
-  int eq = 0;
-  for (int i = lo; i < hi; ++i) eq += key_at(i) == thr;
+  int eq = 0, gt = 0;
+  for (int i = lo; i < hi; ++i) {
+    const uint32_t key = key_at(i);
+    eq += key == thr;
+    gt += key > thr;
+  }
   const int eq_before = block_exclusive_scan(eq, warp_tot, &s_total);
   const int take_eq = min(eq, max(0, need_eq - eq_before));
-  // count kept (global and rank-local)
-  int kept = 0, kept_loc = 0;
-  {
+  const int kept = gt + take_eq;
+  // rank-local count (tensor parallelism only: without it the local list is the global one)
+  int kept_loc = kept;
+  if (!tp1) {
+    kept_loc = 0;
     int te = take_eq;
     for (int i = lo; i < hi; ++i) {
       const uint32_t key = key_at(i);
@@ -180,14 +187,11 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
         keep = true;
         --te;
       }
-      if (keep) {
-        ++kept;
-        kept_loc += tp1 || (i % tp_size) == tp_rank;
-      }
+      if (keep) kept_loc += (i % tp_size) == tp_rank;
     }
   }
   const int pos = block_exclusive_scan(kept, warp_tot, &s_total);
-  const int pos_loc = block_exclusive_scan(kept_loc, warp_tot, &s_total);
+  const int pos_loc = tp1 ? pos : block_exclusive_scan(kept_loc, warp_tot, &s_total);
   if (tid == kTopkThreads - 1 && counts != nullptr) counts[blockIdx.x] = pos_loc + kept_loc;
   const int nw = (f + 31) / 32;
   uint32_t* s_mask = reinterpret_cast<uint32_t*>(hist);  // the histogram is done with
