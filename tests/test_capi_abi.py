@@ -2,7 +2,6 @@
 every entry point include/ffwd_b200.h declares, host-only entry points work,
 and compute entry points fail loudly (no CPU fallback) when there is no GPU."""
 
-import ctypes
 import os
 import re
 

@@ -1,7 +1,6 @@
 """Full prefill (TTFT model of bench.py) with a few layers: target for ncu launch lists."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
 import torch
 import bench
 from paper_2602_00397_b200.prefill import prefill
