@@ -289,3 +289,30 @@ def test_sp_tp2_reduce_scatter_all_gather_matches_reference(sharded):
         h = h + y
     rel = np.linalg.norm(h_tp - h) / np.linalg.norm(h)
     assert rel < 1e-5, rel  # f32 partial sums vs one accumulation: rounding only
+
+
+def test_sharded_predictor_block_ranges():
+    """SeqParallelTP.predicted_blocks: each rank predicts exactly its own blocks minus the
+    prompt's dense first / last block (engine.py:258-262), none under the full-K shortcut
+    (engine.py:268), and the ranks' ranges tile the predicted blocks."""
+    from paper_2602_00397_b200.errors import ValidationError
+    from paper_2602_00397_b200.tp import SeqParallelTP
+    T, d, f = 2048, 64, 256
+    n_blk = T // 128
+    for world in (1, 2, 4, 8):
+        for dfl in (True, False):
+            got = []
+            for rank in range(world):
+                sp = SeqParallelTP([(None, None, 128)], T, d, rank, world, "cpu", comm=None,
+                                   norm_fn=lambda *a: None, ffn_fn=lambda *a: None,
+                                   predict_fn=lambda *a: None, shard_predictor=True, f=f,
+                                   dense_first_last=dfl, x_dtype=torch.float32)
+                lo, hi = sp.predicted_blocks(128)
+                nbr = n_blk // world
+                got += [rank * nbr + b for b in range(lo, hi)]
+                assert sp.predicted_blocks(f) == (0, 0)  # k == d_ffn: every block dense
+            want = list(range(1, n_blk - 1)) if dfl else list(range(n_blk))
+            assert got == want, (world, dfl, got)
+    with pytest.raises(ValidationError):  # rows must be whole blocks per rank
+        SeqParallelTP([(None, None, 128)], 1024, d, 0, 16, "cpu", comm=None,
+                      shard_predictor=True, f=f, x_dtype=torch.float32)
