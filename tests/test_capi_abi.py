@@ -2,6 +2,7 @@
 every entry point include/ffwd_b200.h declares, host-only entry points work,
 and compute entry points fail loudly (no CPU fallback) when there is no GPU."""
 
+import ctypes
 import os
 import re
 
@@ -82,6 +83,33 @@ def test_validation_happens_before_any_launch():
 
 
 @pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU path")
+def test_sequence_parallel_predictor_entries_validate_first():
+    """ffwd_predict_mask / ffwd_ffn_layer_masked reject bad shapes and pointers before
+    any launch (no device needed)."""
+    lib = _lib.load_library()
+    assert lib.ffwd_predict_mask_workspace_bytes(16, 4096, 256, 14336) > 16 * 14336 * 4
+    dummy = ctypes.c_void_p(16)
+    # ld_mask narrower than ceil(f / 32) words
+    rc = lib.ffwd_predict_mask(dummy, 0, 1024, 512, 1, 6, dummy, dummy, dummy, 32, 1376, 688,
+                               None, dummy, 10, dummy, 1 << 30, None)
+    assert rc == _lib.FFWD_ERR_VALIDATION and b"ld_mask" in lib.ffwd_last_error()
+    # blocks outside the tokens
+    rc = lib.ffwd_predict_mask(dummy, 0, 1024, 512, 4, 6, dummy, dummy, dummy, 32, 1376, 688,
+                               None, dummy, 43, dummy, 1 << 30, None)
+    assert rc == _lib.FFWD_ERR_VALIDATION and b"outside" in lib.ffwd_last_error()
+    # null mask
+    rc = lib.ffwd_predict_mask(dummy, 0, 1024, 512, 1, 6, dummy, dummy, dummy, 32, 1376, 688,
+                               None, None, 43, dummy, 1 << 30, None)
+    assert rc == _lib.FFWD_ERR_VALIDATION
+    # masked layer: bad rank, then predicted blocks without (wide enough) mask rows
+    rc = lib.ffwd_ffn_layer_masked(dummy, 1024, 512, dummy, dummy, 688, 32, 1376, 688, 1, 1, 2,
+                                   2, dummy, 43, dummy, None, None, dummy, 1 << 30, None)
+    assert rc == _lib.FFWD_ERR_VALIDATION and b"rank" in lib.ffwd_last_error()
+    rc = lib.ffwd_ffn_layer_masked(dummy, 1024, 512, dummy, dummy, 688, 32, 1376, 688, 1, 1, 0,
+                                   2, dummy, 10, dummy, None, None, dummy, 1 << 30, None)
+    assert rc == _lib.FFWD_ERR_VALIDATION and b"mask" in lib.ffwd_last_error()
+
+
 def test_compute_path_fails_loudly_without_gpu():
     import paper_2602_00397_b200 as ff
     from oracle import ffwd_oracle as orc
