@@ -283,6 +283,15 @@ class TorchComm:
     def all_gather(self, out: torch.Tensor, inp: torch.Tensor) -> None:
         self._run(dist.all_gather_into_tensor, out, inp)
 
+    def all_gather_start(self, out: torch.Tensor, inp: torch.Tensor):
+        """Start an all-gather that overlaps the caller's next kernels (NCCL runs it on its
+        own stream); returns a handle whose ``wait()`` orders the current stream after it.
+        Host-staged (gloo) gathers complete before returning."""
+        if self.staged and out.is_cuda:
+            self.all_gather(out, inp)
+            return None
+        return dist.all_gather_into_tensor(out, inp, group=self.group, async_op=True)
+
     def reduce_scatter(self, out: torch.Tensor, inp: torch.Tensor) -> None:
         self._run(lambda o, i, group: dist.reduce_scatter_tensor(o, i, op=dist.ReduceOp.SUM,
                                                                  group=group), out, inp)
@@ -310,8 +319,9 @@ class SeqParallelTP:
          blocks): the predictor and top-k of this rank's own blocks only
          (``predictor.py:68-81`` is block-local), written as selection bitmasks
          (``layer.predict_mask``: ceil(d_ffn / 32) words per block);
-      3. ``gather``: all-gather x (bf16 [T x d]) and the bitmasks ([n_blk x words]), or,
-         with a replicated predictor, x and the f32 logits;
+      3. ``gather``: all-gather x (bf16 [T x d]; started before ``predict`` so the transfer
+         overlaps the rank's predictor) and the bitmasks ([n_blk x words]), or, with a
+         replicated predictor, x and the f32 logits;
       4. ``ffn``: the FFN branch over all T tokens on this rank's shard: each rank keeps its
          own neurons of every block's selection (``mask_in``; replicated predictor: every
          rank recomputes the same global top-k, bit-exact) -> partial y (f32, or bf16 with
@@ -428,6 +438,9 @@ class SeqParallelTP:
 
     def gather(self) -> None:
         self.comm.all_gather(self.x_full, self.x_shard)
+        self.gather_selection()
+
+    def gather_selection(self) -> None:
         if self.shard_predictor:
             self.comm.all_gather(self.mask_full, self.mask_shard)
         else:
@@ -449,8 +462,16 @@ class SeqParallelTP:
 
     def layer(self, l: int, h_shard: torch.Tensor) -> None:
         self.norm(l, h_shard)
+        # the all-gather of the FFN input (T d bf16, the layer's largest transfer before the
+        # FFN) overlaps this rank's predictor; the small selection gather follows it
+        start = getattr(self.comm, "all_gather_start", None)
+        work = start(self.x_full, self.x_shard) if start else None
+        if start is None:
+            self.comm.all_gather(self.x_full, self.x_shard)
         self.predict(l)
-        self.gather()
+        self.gather_selection()
+        if work is not None:
+            work.wait()
         self.ffn(l)
         self.scatter()
 
