@@ -187,12 +187,13 @@ __global__ void __launch_bounds__(kNormThreads, 2)
 // cross-warp reductions stall the issue slots:
 //   * a producer warp streams the CTA's rows (and the `add` rows) into a shared-memory
 //     ring with 1-D TMA bulk copies, `ns` rows ahead;
-//   * the 8 consumer warps run a two-row software pipeline: phase A of row i (load,
-//     [add], the warp's partial sum of squares, published through an mbarrier) is
-//     followed by phase B of row i - 1 (the row's scale from the 8 partials, outputs,
-//     partial logit), so the wait for the other warps' partials is covered by a row of
-//     work instead of a __syncthreads;
-//   * warp 0 finishes each row's logit two rows later from the warps' partials.
+//   * the 8 consumer warps run a three-row software pipeline: phase A of row i (load,
+//     [add], the warp's partial sum of squares, published through an mbarrier), then
+//     the scale of row i - 1 (f64 divide and square root of the 8 partials, computed
+//     once by the row's owner warp i % 8 and published), then phase B of row i - 2
+//     (outputs, partial logit), so neither the wait for the other warps' partials nor
+//     the scale's dependent f64 chain sits in front of a barrier;
+//   * warp 0 finishes each row's logit three rows later from the warps' partials.
 // Arithmetic per element (the old kernel spent ~46 instructions per element on INT-pipe
 // widening, special-value checks and f64 products; ncu r2):
 //   * ss: one F2F (f32 -> f64, exact) and one DFMA;
@@ -218,6 +219,8 @@ struct RingHdr {
   uint64_t empty[kMaxRing];
   uint64_t bar_ss[kRedSlots];
   uint64_t bar_z[kRedSlots];
+  uint64_t bar_sc[kRedSlots];
+  float sc[kRedSlots][2];  // the row's scale as s_hi, s_lo
   double red_ss[kRedSlots][kRingWarps];
   double red_z[kRedSlots][kRingWarps];
 };
@@ -245,6 +248,7 @@ __global__ void __launch_bounds__(kNormThreads + 32)
     for (int r = 0; r < kRedSlots; ++r) {
       mbar_init(&hd->bar_ss[r], kRingWarps);
       mbar_init(&hd->bar_z[r], kRingWarps);
+      mbar_init(&hd->bar_sc[r], 1);
     }
     fence_barrier_init();
   }
@@ -338,18 +342,33 @@ __global__ void __launch_bounds__(kNormThreads + 32)
     }
   };
 
-  // Phase B: row i's scale, outputs and this warp's partial logit; releases the ring slot.
+  // Row i's scale from the 8 partials, by one owner warp per row (i % 8): the f64
+  // divide and square root are a long dependent chain, so computing them in every warp
+  // cost ~a third of the kernel's instructions and most of its issue-slot latency.
+  auto scale_row = [&](int i) {
+    const int slot = i & (kRedSlots - 1);
+    mbar_wait_sleep(&hd->bar_ss[slot], (i / kRedSlots) & 1, 1000);
+    if (lane == 0) {
+      double ssum = 0.0;
+#pragma unroll
+      for (int w = 0; w < kRingWarps; ++w) ssum += hd->red_ss[slot][w];
+      const double mean = ssum / static_cast<double>(d);
+      const double scale = 1.0 / sqrt(mean + eps);  // kernels.py:105
+      const float s_hi = static_cast<float>(scale);
+      hd->sc[slot][0] = s_hi;
+      hd->sc[slot][1] = static_cast<float>(scale - static_cast<double>(s_hi));
+      mbar_arrive(&hd->bar_sc[slot]);
+    }
+    __syncwarp();
+  };
+
+  // Phase B: row i's outputs and this warp's partial logit; releases the ring slot.
   auto phase_b = [&](int i) {
     const int s = sb, slot = i & (kRedSlots - 1);
     if (++sb == ns) sb = 0;
-    mbar_wait_sleep(&hd->bar_ss[slot], (i / kRedSlots) & 1, 1000);
-    double ssum = 0.0;
-#pragma unroll
-    for (int w = 0; w < kRingWarps; ++w) ssum += hd->red_ss[slot][w];
-    const double mean = ssum / static_cast<double>(d);
-    const double scale = 1.0 / sqrt(mean + eps);  // kernels.py:105
-    const float s_hi = static_cast<float>(scale);
-    const float s_lo = static_cast<float>(scale - static_cast<double>(s_hi));
+    mbar_wait_sleep(&hd->bar_sc[slot], (i / kRedSlots) & 1, 1000);
+    const float s_hi = hd->sc[slot][0];
+    const float s_lo = hd->sc[slot][1];
     const int row = row_of(i);
     const bool want_logit = query != nullptr && row >= logit_row0 && row < logit_row1;
     const float4* xs = reinterpret_cast<const float4*>(ring + static_cast<size_t>(s) * stage_bytes);
@@ -412,17 +431,13 @@ __global__ void __launch_bounds__(kNormThreads + 32)
     __syncwarp();
   };
 
-  for (int i = 0; i < nrows; ++i) {
-    phase_a(i);
-    if (i >= 1) {
-      phase_b(i - 1);
-      if (warp == 0 && i >= 2) finish(i - 2);
-    }
-  }
-  if (nrows >= 1) phase_b(nrows - 1);
-  if (warp == 0) {
-    if (nrows >= 2) finish(nrows - 2);
-    if (nrows >= 1) finish(nrows - 1);
+  // three rows in flight: phase A of row i, the scale of row i - 1 (its owner warp),
+  // phase B of row i - 2, and warp 0 finishing row i - 3's logit
+  for (int i = 0; i < nrows + 3; ++i) {
+    if (i < nrows) phase_a(i);
+    if (i >= 1 && i - 1 < nrows && warp == (i - 1) % kRingWarps) scale_row(i - 1);
+    if (i >= 2 && i - 2 < nrows) phase_b(i - 2);
+    if (warp == 0 && i >= 3 && i - 3 < nrows) finish(i - 3);
   }
 }
 
