@@ -72,6 +72,11 @@ def case_norm():
     torch.cuda.synchronize()
     from paper_2602_00397_b200.predictor import predictor_logits
     assert torch.equal(lg, predictor_logits(dp, xb))
+    # ~10 rows per CTA: the row ring and the reduction slots wrap several times
+    x2 = torch.randn((3000, d), device="cuda")
+    xb2, _, lg2 = rmsnorm(x2, torch.ones(d, device="cuda"), predictor=dp)
+    torch.cuda.synchronize()
+    assert torch.equal(lg2, predictor_logits(dp, xb2))
     print("norm: ok")
 
 
