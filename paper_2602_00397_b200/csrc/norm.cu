@@ -243,10 +243,10 @@ __global__ void __launch_bounds__(kNormThreads + 32)
   if (threadIdx.x == 0) {
     for (int s = 0; s < ns; ++s) {
       mbar_init(&hd->full[s], 1);
-      mbar_init(&hd->empty[s], kRingWarps);
+      mbar_init(&hd->empty[s], kNormThreads);  // every consumer thread releases the slot
     }
     for (int r = 0; r < kRedSlots; ++r) {
-      mbar_init(&hd->bar_ss[r], kRingWarps);
+      mbar_init(&hd->bar_ss[r], kNormThreads);
       mbar_init(&hd->bar_z[r], kRingWarps);
       mbar_init(&hd->bar_sc[r], 1);
     }
@@ -336,10 +336,10 @@ __global__ void __launch_bounds__(kNormThreads + 32)
       }
     }
     const double ss = rowdot::warp_sum(rowdot::thread_value(sq));
-    if (lane == 0) {
-      hd->red_ss[i & (kRedSlots - 1)][warp] = ss;
-      mbar_arrive(&hd->bar_ss[i & (kRedSlots - 1)]);
-    }
+    if (lane == 0) hd->red_ss[i & (kRedSlots - 1)][warp] = ss;
+    // every lane arrives: its earlier reads of the slot's scale (row i - 4) are then
+    // ordered before the owner's next write of it
+    mbar_arrive(&hd->bar_ss[i & (kRedSlots - 1)]);
   };
 
   // Row i's scale from the 8 partials, by one owner warp per row (i % 8): the f64
@@ -408,8 +408,7 @@ __global__ void __launch_bounds__(kNormThreads + 32)
       }
     }
     if constexpr (kAdd != 0) fence_proxy_async_smem();  // phase A wrote into the slot
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&hd->empty[s]);
+    mbar_arrive(&hd->empty[s]);  // each thread's reads of the slot precede the refill
     const double zs = want_logit ? rowdot::warp_sum(rowdot::thread_value(z)) : 0.0;
     if (lane == 0) {
       hd->red_z[slot][warp] = zs;
