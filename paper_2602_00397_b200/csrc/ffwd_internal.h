@@ -87,6 +87,7 @@ cudaError_t launch_rope(void* qk, bool is_f32, int T, int row_stride, int k_col,
                         const float* sin32, int pos0, cudaStream_t s);
 // `partial` (nullable, gemm_f64acc_partial_bytes) enables split-K for long K.
 size_t gemm_f64acc_partial_bytes(int M, int K, int N);
+int gemm_f64acc_kernels(int M, int K, int N, bool has_partial);  // launches per call
 cudaError_t launch_gemm_f64acc(const float* A, const float* B, float* C, int M, int K, int N,
                                bool relu, double* partial, cudaStream_t s);
 // `mask` (nullable): also the selection bitmask of each row (ld_mask 32-bit words per row)

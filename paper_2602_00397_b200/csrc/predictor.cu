@@ -26,6 +26,8 @@
 #include "ffwd_internal.h"
 #include "launch.cuh"
 
+#include <cooperative_groups.h>
+
 // pooled_kernel tuning: tokens in flight per lane (bf16) and the CTAs-per-SM register bound
 #ifndef FFWD_POOL_BATCH
 #define FFWD_POOL_BATCH 8
@@ -38,6 +40,8 @@
 #include "sm100.cuh"
 
 namespace ffwd {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -563,6 +567,117 @@ __global__ void __launch_bounds__(GTHREADS)
   }
 }
 
+// Split-K for short prompts (M <= 64 rows: the 1B shape's W1, a sequence shard's blocks):
+// the K splits of one output tile run as one thread-block cluster (grid.x = splits) and
+// are summed through distributed shared memory in split order, s = 0 + p_0 + p_1 + ...
+// -- the gemm_reduce_kernel order, so no f64 partial round trip through global memory and
+// no second launch.  Tiles are 32 RG rows x 32 columns (no padding of 32 rows to 128);
+// warp w takes row group w % RG and 8 (RG = 1) or 16 (RG = 2) columns, each element
+// accumulated in the same k order as gemm_f64_kernel.
+constexpr int kCzBN = 32;
+template <int RG>
+__global__ void __launch_bounds__(GTHREADS)
+    gemm_f64_cluster_kernel(const float* __restrict__ A, const float* __restrict__ B,
+                            float* __restrict__ C, int M, int K, int N, int kper, int relu) {
+  constexpr int BM = 32 * RG;
+  constexpr int AP = GBK + 4;
+  constexpr int BP = kCzBN + 8;
+  constexpr int WC = kCzBN / (4 / RG);  // columns per warp
+  constexpr int NJ = WC / 8;
+  __shared__ __align__(16) float As[2][BM * AP];
+  __shared__ __align__(16) float Bs[2][GBK * BP];
+  __shared__ __align__(16) double part[BM * kCzBN];
+  cg::cluster_group cl = cg::this_cluster();
+  const int z = static_cast<int>(cl.block_rank()), nz = static_cast<int>(cl.num_blocks());
+  pdl_wait();
+  pdl_trigger();
+  const int n0 = blockIdx.y * kCzBN, m0 = blockIdx.z * BM;
+  const int k_lo = z * kper, k_hi = min(K, k_lo + kper);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int rg = warp % RG, wc = (warp / RG) * WC;
+  const bool vec = (K & 3) == 0 && (N & 3) == 0;
+
+  auto load_chunk = [&](int buf, int k0) {
+    for (int e = threadIdx.x; e < BM * (GBK / 4); e += GTHREADS) {
+      const int r = e / (GBK / 4), c = (e % (GBK / 4)) * 4;
+      const int gm = m0 + r, gk = k0 + c;
+      float* dst = &As[buf][r * AP + c];
+      const float* src = A + static_cast<size_t>(gm) * K + gk;
+      if (vec && gm < M && gk + 3 < k_hi) {
+        cp_async16(dst, src);
+      } else {
+        for (int u = 0; u < 4; ++u) dst[u] = (gm < M && gk + u < k_hi) ? __ldg(src + u) : 0.f;
+      }
+    }
+    for (int e = threadIdx.x; e < GBK * (kCzBN / 4); e += GTHREADS) {
+      const int r = e / (kCzBN / 4), c = (e % (kCzBN / 4)) * 4;
+      const int gk = k0 + r, gn = n0 + c;
+      float* dst = &Bs[buf][r * BP + c];
+      const float* src = B + static_cast<size_t>(gk) * N + gn;
+      if (vec && gk < k_hi && gn + 3 < N) {
+        cp_async16(dst, src);
+      } else {
+        for (int u = 0; u < 4; ++u) dst[u] = (gk < k_hi && gn + u < N) ? __ldg(src + u) : 0.f;
+      }
+    }
+    cp_async_commit();
+  };
+
+  double acc[4][NJ][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  int buf = 0;
+  if (k_lo < k_hi) load_chunk(0, k_lo);
+  for (int k0 = k_lo; k0 < k_hi; k0 += GBK) {
+    if (k0 + GBK < k_hi) {
+      load_chunk(buf ^ 1, k0 + GBK);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const float* as = As[buf];
+    const float* bs = Bs[buf];
+#pragma unroll
+    for (int ks = 0; ks < GBK / 4; ++ks) {
+      double a[4], bb[NJ];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        a[i] = static_cast<double>(as[(32 * rg + 8 * i + fr) * AP + 4 * ks + fc]);
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) bb[j] = static_cast<double>(bs[(4 * ks + fc) * BP + wc + 8 * j + fr]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j], a[i], bb[j]);
+    }
+    __syncthreads();
+    buf ^= 1;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        part[(32 * rg + 8 * i + fr) * kCzBN + wc + 8 * j + 2 * fc + h] = acc[i][j][h];
+  cl.sync();  // every split's partial tile is in its shared memory
+  for (int e = z * GTHREADS + threadIdx.x; e < BM * kCzBN; e += nz * GTHREADS) {
+    const int gm = m0 + e / kCzBN, gn = n0 + e % kCzBN;
+    double s = 0.0;
+    for (int q = 0; q < nz; ++q) s += *cl.map_shared_rank(&part[e], q);  // split order
+    if (gm < M && gn < N) {
+      float v = static_cast<float>(s);
+      if (relu) v = fmaxf(v, 0.0f);  // predictor.py:79: relu after the f32 rounding
+      C[static_cast<size_t>(gm) * N + gn] = v;
+    }
+  }
+  cl.sync();  // no CTA leaves while its partial tile may still be read
+}
+
 __global__ void gemm_reduce_kernel(const double* __restrict__ partial, float* __restrict__ C,
                                    int MN, int splits, int relu) {
   pdl_wait();
@@ -585,6 +700,12 @@ __global__ void gemm_reduce_kernel(const double* __restrict__ partial, float* __
 #ifndef FFWD_MAX_SPLITS
 #define FFWD_MAX_SPLITS 32
 #endif
+// h-resident scores GEMM from this many output columns (M <= 64 rows): the 1B shape's
+// 32 x 8192 scores take 128 CTAs of 32-row tiles instead of 128-row tiles 3/4 padding
+#ifndef FFWD_RESIDENT_MIN_N
+#define FFWD_RESIDENT_MIN_N 4096
+#endif
+constexpr int kResidentMinN = FFWD_RESIDENT_MIN_N;
 constexpr int kGemmBN = FFWD_SPLIT_BN;
 constexpr int kMaxSplits = FFWD_MAX_SPLITS;
 
@@ -650,12 +771,53 @@ cudaError_t launch_logits_only(const void* x, bool x_is_f32, int d, int tok0, in
 template <int RG>
 cudaError_t launch_resident(const float* A, const float* B, float* C, int M, int K, int N,
                             bool relu, size_t smem, int grid, cudaStream_t s) {
-  static std::atomic<uint64_t> attr{0};  // one per instantiation: each kernel needs its own
-  if (cudaError_t e = ensure_smem_limit(gemm_f64_resident_kernel<RG>, smem, attr);
+  // one per instantiation: each kernel needs its own.  The limit is raised to the most any
+  // call may ask for (200 KiB), not this call's size: the attribute is set only once.
+  static std::atomic<uint64_t> attr{0};
+  if (cudaError_t e = ensure_smem_limit(gemm_f64_resident_kernel<RG>, 200 * 1024, attr);
       e != cudaSuccess)
     return e;
   return launch_k(gemm_f64_resident_kernel<RG>, dim3(grid), dim3(GTHREADS), smem, s, 1, A, B, C,
                   M, K, N, relu ? 1 : 0);
+}
+
+// The cluster split-K path (gemm_f64_cluster_kernel): M <= 64, at most kCzMax splits.
+#ifndef FFWD_CLUSTER_SPLITK
+#define FFWD_CLUSTER_SPLITK 1
+#endif
+constexpr int kCzMax = 16;  // non-portable cluster size (B200 allows 16)
+int cluster_splits(int M, int K, int N) {
+  if (!FFWD_CLUSTER_SPLITK || M > 64 || N >= kResidentMinN) return 1;
+  const int tiles = ((N + kCzBN - 1) / kCzBN) * ((M + 31) / 32);
+  int splits = 1;
+  while (tiles * splits < 2 * 148 && K / (2 * splits) >= 2 * GBK && splits < kCzMax) splits *= 2;
+  return splits;
+}
+
+template <int RG>
+cudaError_t launch_cluster_splitk(const float* A, const float* B, float* C, int M, int K, int N,
+                                  bool relu, int splits, cudaStream_t s) {
+  static std::atomic<uint64_t> done{0};
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (!(done.load(std::memory_order_acquire) & bit)) {
+    if (cudaError_t e = cudaFuncSetAttribute(gemm_f64_cluster_kernel<RG>,
+                                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        e != cudaSuccess)
+      return e;
+    done.fetch_or(bit, std::memory_order_acq_rel);
+  }
+  const int kper = ((K + splits - 1) / splits + GBK - 1) / GBK * GBK;
+  const int z = (K + kper - 1) / kper;
+  const dim3 grid(z, (N + kCzBN - 1) / kCzBN, (M + 32 * RG - 1) / (32 * RG));
+  return launch_k(gemm_f64_cluster_kernel<RG>, grid, dim3(GTHREADS), 0, s, z, A, B, C, M, K, N,
+                  kper, relu ? 1 : 0);
+}
+
+int gemm_f64acc_kernels(int M, int K, int N, bool has_partial) {
+  if (!has_partial || cluster_splits(M, K, N) > 1) return 1;
+  return gemm_splits(M, K, N) > 1 ? 2 : 1;
 }
 
 size_t gemm_f64acc_partial_bytes(int M, int K, int N) {
@@ -666,6 +828,11 @@ size_t gemm_f64acc_partial_bytes(int M, int K, int N) {
 cudaError_t launch_gemm_f64acc(const float* A, const float* B, float* C, int M, int K, int N,
                                bool relu, double* partial, cudaStream_t s) {
   if (M <= 0 || N <= 0) return cudaSuccess;
+  if (partial) {
+    if (const int cz = cluster_splits(M, K, N); cz > 1)
+      return M > 32 ? launch_cluster_splitk<2>(A, B, C, M, K, N, relu, cz, s)
+                    : launch_cluster_splitk<1>(A, B, C, M, K, N, relu, cz, s);
+  }
   const int splits = partial ? gemm_splits(M, K, N) : 1;
   const int kper = ((K + splits - 1) / splits + GBK - 1) / GBK * GBK;
   const int z = (K + kper - 1) / kper;
@@ -674,7 +841,7 @@ cudaError_t launch_gemm_f64acc(const float* A, const float* B, float* C, int M, 
   // h resident for up to 64 rows (a sequence shard's or a short prompt's blocks); at 128
   // rows the resident tile leaves one 4-warp CTA per SM and runs slower (83 vs 54 us at
   // 8B/16K), so full prompts keep the 16-column tiles below.
-  if (z == 1 && N >= 16 * 4 * 148 && M <= 64 && K % GBK == 0 && N % 4 == 0) {
+  if (N >= kResidentMinN && M <= 64 && K % GBK == 0 && N % 4 == 0) {
     const int rg = M > 32 ? 2 : 1;
     const size_t smem = (static_cast<size_t>(32 * rg) * (K + 4) +
                          2 * GBK * (16 * (4 / rg) + 8)) * sizeof(float);

@@ -108,6 +108,40 @@ def test_topk_tp_local_lists(ff):
                 np.testing.assert_array_equal(loc[r, :cnt[r]], mine)
 
 
+def test_topk_widths_ties_and_tp(ff):
+    """Top-k over rows of 2K-32K scores: widths that are not multiples of the thread count,
+    ties spread over the whole row (one giant tie, duplicated halves, -0 / NaN), k at
+    1 / f-1 / f, and the global list plus the rank-local lists + counts under TP."""
+    from paper_2602_00397_b200 import _dev, _lib
+    rng = np.random.default_rng(11)
+    for f in (2048, 2052, 4100, 8192, 12288, 14336, 30000, 32768):
+        rows = 5
+        s = rng.standard_normal((rows, f)).astype(np.float32)
+        s[1] = np.round(s[1] * 2) / 2          # few distinct values: ties across chunks
+        s[2] = 0.0                              # one giant tie
+        s[2, ::5] = -0.0
+        s[3, ::3] = np.nan
+        s[4, f // 2:] = s[4, :f - f // 2]       # duplicated halves
+        st = torch.from_numpy(s).cuda()
+        lib = _dev.lib_for(st.device)
+        for k in (1, 7, f // 3, f // 2, f - 1, f):
+            for tp, rank in ((1, 0), (2, 1), (8, 5)):
+                kl = min(k, (f + tp - 1) // tp)
+                glob = torch.full((rows, k), -1, dtype=torch.int32, device="cuda")
+                loc = torch.full((rows, kl), -1, dtype=torch.int32, device="cuda")
+                cnt = torch.zeros(rows, dtype=torch.int32, device="cuda")
+                _lib.check(lib.ffwd_topk(st.data_ptr(), rows, f, k, rank, tp, glob.data_ptr(), k,
+                                         loc.data_ptr(), kl, cnt.data_ptr(),
+                                         _dev.stream_handle(st.device)), "topk")
+                g, lc, c = glob.cpu().numpy(), loc.cpu().numpy(), cnt.cpu().numpy()
+                for r in range(rows):
+                    full = orc.topk_indices(s[r], k)
+                    np.testing.assert_array_equal(g[r], full, err_msg=f"f={f} k={k} row {r}")
+                    mine = full[full % tp == rank] // tp
+                    assert c[r] == mine.size, (f, k, tp, r)
+                    np.testing.assert_array_equal(lc[r, :c[r]], mine)
+
+
 def _layer_case(ff, name):
     c = load_case(name)
     lw = c["lw"]
