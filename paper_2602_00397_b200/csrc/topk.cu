@@ -59,6 +59,32 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot, int* t
   return r;
 }
 
+// The same scan over 64-bit values (two packed 32-bit counts); no total.
+__device__ __forceinline__ unsigned long long block_exclusive_scan64(unsigned long long v,
+                                                                     unsigned long long* wtot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wtot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const unsigned long long wv = wtot[lane];
+    unsigned long long wi = wv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    wtot[lane] = wi - wv;
+  }
+  __syncthreads();
+  return wtot[warp] + incl - v;
+}
+
 // Radix digits, most significant first: 12 + 12 + 8 bits.  A 12-bit first digit
 // spreads scores of similar magnitude (same sign and exponent) over many bins, which
 // keeps the shared-memory histogram atomics nearly conflict free.
@@ -78,35 +104,51 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
     int32_t* __restrict__ idx_global, int ld_global, int32_t* __restrict__ idx_local,
     int ld_local, int32_t* __restrict__ counts, uint32_t* __restrict__ mask, int ld_mask) {
   extern __shared__ uint32_t s_keys[];
-  __shared__ int hist[kBins];
+  // two histograms: pass 1 builds hist[1] while pass 0's is still being searched, and
+  // pass 2 reuses hist[0] (zeroed during pass 1), so no pass waits on a separate zeroing
+  __shared__ __align__(16) int hist[2][kBins];
   __shared__ int warp_tot[32];
+  __shared__ unsigned long long warp_tot64[32];
   __shared__ int s_total;
   __shared__ uint32_t s_prefix;
   __shared__ int s_remaining;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {
+    int4* h4 = reinterpret_cast<int4*>(&hist[0][0]);
+    for (int i = tid; i < 2 * kBins / 4; i += kTopkThreads) h4[i] = make_int4(0, 0, 0, 0);
+  }
   pdl_wait();
   pdl_trigger();
   const float* s = scores + static_cast<size_t>(blockIdx.x) * f;
-  const int tid = threadIdx.x;
   auto key_at = [&](int i) -> uint32_t {
     if constexpr (kCached) return s_keys[i];
     else return rank_key(__ldg(s + i));
   };
+  __syncthreads();
   if constexpr (kCached) {
     // the first pass's histogram (top 12 bits, every key counts) is built while staging
-    for (int i = tid; i < kBins; i += kTopkThreads) hist[i] = 0;
-    __syncthreads();
     auto stage = [&](int i, uint32_t key) {
       s_keys[i] = key;
-      atomicAdd(&hist[key >> digit_shift(0)], 1);
+      atomicAdd(&hist[0][key >> digit_shift(0)], 1);
     };
     if ((f & 3) == 0) {
+      // four 16 B loads in flight per thread before the first histogram atomic
       const float4* s4 = reinterpret_cast<const float4*>(s);
-      for (int i = tid; i < f / 4; i += kTopkThreads) {
-        const float4 v = __ldg(s4 + i);
-        stage(4 * i, rank_key(v.x));
-        stage(4 * i + 1, rank_key(v.y));
-        stage(4 * i + 2, rank_key(v.z));
-        stage(4 * i + 3, rank_key(v.w));
+      const int n4 = f / 4;
+      for (int i0 = tid; i0 < n4; i0 += 4 * kTopkThreads) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (i0 + u * kTopkThreads < n4) v[u] = __ldg(s4 + i0 + u * kTopkThreads);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * kTopkThreads;
+          if (i >= n4) break;
+          stage(4 * i, rank_key(v[u].x));
+          stage(4 * i + 1, rank_key(v[u].y));
+          stage(4 * i + 2, rank_key(v[u].z));
+          stage(4 * i + 3, rank_key(v[u].w));
+        }
       }
     } else {
       for (int i = tid; i < f; i += kTopkThreads) stage(i, rank_key(__ldg(s + i)));
@@ -119,50 +161,74 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
   for (int pass = 0; pass < 3; ++pass) {
     const int shift = digit_shift(pass);
     const int nb = 1 << digit_bits(pass);
+    int* h = hist[pass & 1];
+    if (pass == 1)  // pass 2's histogram: hist[0] was last read before the previous barrier
+      for (int i = tid; i < (1 << digit_bits(2)); i += kTopkThreads) hist[0][i] = 0;
     if (!kCached || pass > 0) {  // cached: pass 0's histogram came with the staging
-      for (int i = tid; i < nb; i += kTopkThreads) hist[i] = 0;
-      __syncthreads();
       for (int i = tid; i < f; i += kTopkThreads) {
         const uint32_t key = key_at(i);
-        if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & (nb - 1)], 1);
+        if ((key & pmask) == prefix) atomicAdd(&h[(key >> shift) & (nb - 1)], 1);
       }
     }
     __syncthreads();
-    // thread t owns bins [nb-1-B t-(B-1), nb-1-B t] (descending); block scan finds the
-    // bin holding the remaining-th largest key
-    const int B = (nb + kTopkThreads - 1) / kTopkThreads;
+    // warp w owns bins [nb-1-bpw w-(bpw-1), nb-1-bpw w] in descending order, bpl per lane;
+    // warp totals are scanned by every warp, and only the warp holding the
+    // remaining-th largest key scans its lanes -- two barriers per pass
+    const int bpw = nb / 32;
+    const int bpl = bpw >= 32 ? bpw / 32 : 1;
+    const int top = nb - 1 - bpw * warp - bpl * lane;
+    const bool lane_on = bpl * lane < bpw;
     int c[kBinsPerThread], lsum = 0;
 #pragma unroll
     for (int j = 0; j < kBinsPerThread; ++j) {
-      const int bin = nb - 1 - B * tid - j;
-      c[j] = (j < B && bin >= 0) ? hist[bin] : 0;
+      c[j] = (lane_on && j < bpl) ? h[top - j] : 0;
       lsum += c[j];
     }
-    const int above = block_exclusive_scan(lsum, warp_tot, &s_total);
-    if (above < remaining && above + lsum >= remaining) {
-      int cum = above, bin = nb - 1 - B * tid;
+    int incl = lsum;
 #pragma unroll
-      for (int j = 0; j < kBinsPerThread; ++j) {
-        if (j < B && cum + c[j] >= remaining) {
-          bin = nb - 1 - B * tid - j;
-          break;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    const int wt = warp_tot[lane];
+    int winc = wt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, winc, o);
+      if (lane >= o) winc += t;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, winc >= remaining);
+    const int wb = hit ? __ffs(hit) - 1 : 31;
+    const int above_w = __shfl_sync(0xffffffffu, winc - wt, wb);
+    if (warp == wb) {
+      const int above = above_w + incl - lsum;
+      if (lane_on && above < remaining && above + lsum >= remaining) {
+        int cum = above, bin = top;
+#pragma unroll
+        for (int j = 0; j < kBinsPerThread; ++j) {
+          if (j < bpl && cum + c[j] >= remaining) {
+            bin = top - j;
+            break;
+          }
+          cum += c[j];
         }
-        cum += c[j];
+        s_prefix = prefix | (static_cast<uint32_t>(bin) << shift);
+        s_remaining = remaining - cum;
       }
-      s_prefix = prefix | (static_cast<uint32_t>(bin) << shift);
-      s_remaining = remaining - cum;
     }
     __syncthreads();
     prefix = s_prefix;
     remaining = s_remaining;
     pmask |= static_cast<uint32_t>(nb - 1) << shift;
-    __syncthreads();
   }
   const uint32_t thr = prefix;    // key of the k-th largest score
   const int need_eq = remaining;  // how many keys == thr to keep (lowest index first)
 
   // -- compaction in index order: contiguous chunk per thread.  One pass counts the keys
-  // above the threshold and the ties; the ties are taken lowest index first.
+  // above the threshold and the ties, and one scan of (gt, eq) gives both the tie quota and
+  // the output position: the ties taken before thread t are min(need_eq, eq_before).
   const bool tp1 = tp_size == 1;
   const int per = (f + kTopkThreads - 1) / kTopkThreads;
   const int lo = min(f, tid * per), hi = min(f, lo + per);
@@ -172,9 +238,13 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
     eq += key == thr;
     gt += key > thr;
   }
-  const int eq_before = block_exclusive_scan(eq, warp_tot, &s_total);
+  const unsigned long long before = block_exclusive_scan64(
+      (static_cast<unsigned long long>(gt) << 32) | static_cast<unsigned>(eq), warp_tot64);
+  const int eq_before = static_cast<int>(before & 0xffffffffu);
+  const int gt_before = static_cast<int>(before >> 32);
   const int take_eq = min(eq, max(0, need_eq - eq_before));
   const int kept = gt + take_eq;
+  const int pos = gt_before + min(need_eq, eq_before);
   // rank-local count (tensor parallelism only: without it the local list is the global one)
   int kept_loc = kept;
   if (!tp1) {
@@ -190,11 +260,10 @@ __global__ void __launch_bounds__(kTopkThreads) topk_kernel(
       if (keep) kept_loc += (i % tp_size) == tp_rank;
     }
   }
-  const int pos = block_exclusive_scan(kept, warp_tot, &s_total);
   const int pos_loc = tp1 ? pos : block_exclusive_scan(kept_loc, warp_tot, &s_total);
   if (tid == kTopkThreads - 1 && counts != nullptr) counts[blockIdx.x] = pos_loc + kept_loc;
   const int nw = (f + 31) / 32;
-  uint32_t* s_mask = reinterpret_cast<uint32_t*>(hist);  // the histogram is done with
+  uint32_t* s_mask = reinterpret_cast<uint32_t*>(&hist[0][0]);  // the histograms are done with
   if (mask) {
     for (int i = tid; i < nw; i += kTopkThreads) s_mask[i] = 0u;
     __syncthreads();
@@ -279,7 +348,7 @@ __global__ void __launch_bounds__(kTopkThreads) mask_to_local_kernel(
   }
 }
 
-constexpr size_t kTopkMaxSmem = 200 * 1024;
+constexpr size_t kTopkMaxSmem = 190 * 1024;  // + 33 KiB of static histograms
 
 }  // namespace
 
