@@ -42,6 +42,11 @@
 #ifdef FFWD_K3_A_LDGSTS
 #define FFWD_A_LDGSTS
 #endif
+// FFWD_K3_B_LDGSTS: the gathered W_down rows by 16 B cp.async from all producer lanes
+// instead of TMA tile::gather4 (contiguous stages keep their 2-D TMA boxes)
+#ifdef FFWD_K3_B_LDGSTS
+#define FFWD_B_LDGSTS
+#endif
 // Dynamic tile claiming (FFWD_K3_DYN, default on): gemm_sm100.cuh TileQueue.
 #ifndef FFWD_K3_DYN
 #define FFWD_K3_DYN 1
@@ -188,7 +193,41 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (lane < Q) rows[lane] = cur;
         __syncwarp();
-        if (lane == 0) {
+        if constexpr (kBLdgsts) {
+          static_assert(kSplit, "B by cp.async needs the split A ring");
+          if (lane == 0) mbar_wait(&sm.bar->empty[stage], phase ^ 1);
+          __syncwarp();
+          if (contiguous) {
+            if (warp == 0 && lane == 0) {
+              mbar_arrive_expect_tx(&sm.bar->full[stage], BK * BN * 2);
+              if (kb == 0 && a.blk_done) wait_block_h(a.blk_done + tl.b, m.n_up);
+              const int r0 = m.idx_row < 0 ? kr * BK : a.f_local + (kr * BK - m.kpad);
+#pragma unroll
+              for (int c = 0; c < kChunks; ++c)
+                tma_load_2d(&tm_wt, &sm.bar->full[stage], sm.b_stage(stage) + c * kLbo,
+                            tl.n0 + c * 64, r0, pol_w);
+            } else {
+              mbar_arrive(&sm.bar->full[stage]);
+            }
+          } else {
+            // lane l copies 16 B chunks l, l+32, ... of the warp's Q row segments (BN = 256:
+            // one whole row per warp instruction, coalesced), into the swizzled MN-major
+            // atoms: chunk j of column atom c of K row pos at c*LBO + (pos/8)*1024 +
+            // (pos%8)*128 + ((j ^ pos%8) * 16), where the tensor map's 128B swizzle puts it
+            constexpr int kRowChunks = BN / 8;
+            const __nv_bfloat16* wd = static_cast<const __nv_bfloat16*>(a.wd);
+#pragma unroll
+            for (int q = static_cast<int>(lane); q < Q * kRowChunks; q += 32) {
+              const int i = q / kRowChunks, cc = q % kRowChunks, c = cc >> 3, j = cc & 7;
+              const int pos = Q * warp + i;
+              uint8_t* dst = sm.b_stage(stage) + c * kLbo + (pos >> 3) * 1024 +
+                             (pos & 7) * 128 + ((j ^ (pos & 7)) << 4);
+              cp_async_cg16(dst, wd + static_cast<size_t>(rows[i]) * a.d + tl.n0 + c * 64 +
+                                     j * 8);
+            }
+            cp_async_arrive_noinc(&sm.bar->full[stage]);
+          }
+        } else if (lane == 0) {
           mbar_wait(&sm.bar->empty[stage], phase ^ 1);
           uint32_t nbytes = contiguous ? 0 : Q * BN * 2;
           if (warp == 0) nbytes += (kSplit ? 0 : kABytes) + (contiguous ? BK * BN * 2 : 0);

@@ -80,6 +80,16 @@ constexpr uint32_t kALanes = 32;
 constexpr bool kALdgsts = false;
 constexpr uint32_t kALanes = 1;
 #endif
+// FFWD_B_LDGSTS (per kernel TU, K3 only): the gathered B rows are copied by every producer
+// lane with 16 B cp.async into the 128B-swizzled layout instead of TMA tile::gather4, so
+// the row gathers bypass the SM's TMA unit; full[] then counts one arrival per lane.
+#ifdef FFWD_B_LDGSTS
+constexpr bool kBLdgsts = true;
+constexpr uint32_t kBLanes = 32;
+#else
+constexpr bool kBLdgsts = false;
+constexpr uint32_t kBLanes = 1;
+#endif
 constexpr int kABytes = BM * BK * 2;  // 16 KiB
 
 __host__ __device__ constexpr int round_up(int v, int m) { return (v + m - 1) / m * m; }
@@ -245,7 +255,7 @@ template <int kBBytes>
 __device__ __forceinline__ void prologue(Smem<kBBytes>& sm, int warp) {
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStagesB; ++i) {
-      mbar_init(&sm.bar->full[i], kProducerWarps);
+      mbar_init(&sm.bar->full[i], kProducerWarps * kBLanes);
       mbar_init(&sm.bar->empty[i], 1);
     }
     for (int i = 0; i < kStagesA; ++i) {
@@ -350,7 +360,7 @@ __device__ __forceinline__ void mma_tile_split(Smem<kBBytes>& sm, uint32_t tmem_
     mbar_wait(&sm.bar->fullA[sa], pa);
     mbar_wait(&sm.bar->full[sb], pb);
 #endif
-    if constexpr (kALdgsts) fence_proxy_async_smem();  // cp.async (generic proxy) -> UMMA
+    if constexpr (kALdgsts || kBLdgsts) fence_proxy_async_smem();  // cp.async (generic) -> UMMA
     tc_fence_after();
     const uint64_t adesc = make_sdesc_sw128(smem_u32(sm.a_stage(sa)), 16, 1024);
     const uint64_t bdesc = make_sdesc_sw128(smem_u32(sm.b_stage(sb)), b_lbo, b_sbo);
