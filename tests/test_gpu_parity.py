@@ -64,6 +64,28 @@ def test_predictor_scores_and_indices_bit_exact(ff, name):
         np.testing.assert_array_equal(idx, c["indices"])
 
 
+@pytest.mark.parametrize("d,r,f,n_blk", [(256, 16, 1376, 1), (1024, 64, 3000, 31),
+                                          (2048, 128, 4096, 33), (4096, 256, 2048, 64),
+                                          (1000, 64, 2500, 7), (2048, 128, 8192, 65)])
+def test_predictor_short_prompt_paths_bit_exact(ff, d, r, f, n_blk):
+    """The predictor GEMM paths of short prompts (<= 64 blocks: W1's split-K summed in a
+    thread-block cluster, 32- / 64-row tiles, the h-resident scores GEMM from 4096 columns)
+    and their neighbours (65 blocks: the 128-row split-K path): scores bit-identical to the
+    oracle (predictor.py:68-81) for every block, both input dtypes, odd d / r / f / counts."""
+    rng = np.random.default_rng(d + r + f + n_blk)
+    pred = orc.init_predictor(rng, d, f, r)
+    T = 128 * n_blk - 37 if n_blk > 1 else 128  # a short tail block
+    x = orc.bf16_round(rng.standard_normal((T, d)).astype(np.float32))
+    dp = dev_pred(ff, pred)
+    want = np.stack([orc.predictor_forward(pred["query"], pred["w1"], pred["w2"],
+                                           x[128 * b:min(T, 128 * b + 128)])
+                     for b in range(n_blk)])
+    for dtype in (torch.bfloat16, torch.float32):
+        got = ff.predictor_scores(dp, torch.from_numpy(x).to("cuda", dtype)).cpu().numpy()
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32),
+                                      err_msg=f"{dtype}")
+
+
 def test_topk_edge_cases_match_reference(ff):
     from paper_2602_00397_b200.sparse import topk_device
     g = golden("topk_edges")
