@@ -1,7 +1,7 @@
 """Small cases for compute-sanitizer (memcheck / racecheck / synccheck): every hot-path
 kernel at parity sizes, checked against the oracle so a silent corruption also fails.
 
-  cfg1   one predicted layer (d512 f1376 T1024): logits/pool, W1 split-K + reduce, W2,
+  cfg1   one predicted layer (d512 f1376 T1024): logits/pool, W1 cluster split-K (DSMEM), W2,
          top-k, plan, K2 (CTA pairs, multicast), K3 (per-block K2->K3 counters, PDL)
   edge   short / single-token blocks, k = 1, k = f - 1, ragged compensator, 64-col tiles
   norm   the FFN-input RMSNorm with fused logits and residual add
