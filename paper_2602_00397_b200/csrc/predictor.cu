@@ -28,6 +28,10 @@
 
 #include <cooperative_groups.h>
 
+// pooled_kernel: 256-column CTAs when the 512-column grid has fewer CTAs than this (0: never)
+#ifndef FFWD_POOL_NARROW_BELOW
+#define FFWD_POOL_NARROW_BELOW 148
+#endif
 // pooled_kernel tuning: tokens in flight per lane (bf16) and the CTAs-per-SM register bound
 #ifndef FFWD_POOL_BATCH
 #define FFWD_POOL_BATCH 8
@@ -214,12 +218,16 @@ __global__ void __launch_bounds__(kBlockTokens)
 #ifndef FFWD_POOL_F2F
 #define FFWD_POOL_F2F 1
 #endif
-template <bool kF32>
+// kHalves = 2: 512 columns per CTA (8 warps); 1: 256 columns (4 warps), for grids under
+// one wave (short prompts: twice the CTAs).  Each column's sum is the same either way.
+template <bool kF32, int kHalves>
 __global__ void __launch_bounds__(kPoolThreads, FFWD_POOL_MINB)
     pooled_kernel(const void* __restrict__ x, int T, int d, int blk_begin, int blk_count,
                   const float* __restrict__ probs, float* __restrict__ pooled) {
+  constexpr int kCols = 256 * kHalves;
+  constexpr int kThr = 128 * kHalves;
   __shared__ double probd[kBlockTokens];
-  __shared__ double red[kPoolQuarters][kPoolCols];
+  __shared__ double red[kPoolQuarters][kCols];
   pdl_wait();
   pdl_trigger();
   const int rel = blk_count - 1 - static_cast<int>(blockIdx.y);
@@ -230,9 +238,9 @@ __global__ void __launch_bounds__(kPoolThreads, FFWD_POOL_MINB)
     probd[threadIdx.x] = static_cast<double>(probs[rel * kBlockTokens + threadIdx.x]);
   __syncthreads();
 
-  const int half = warp & 1, quarter = warp >> 1;
-  const int cl = half * 256 + lane * 8;  // column within the CTA's 512
-  const int c = blockIdx.x * kPoolCols + cl;
+  const int half = kHalves == 2 ? warp & 1 : 0, quarter = kHalves == 2 ? warp >> 1 : warp;
+  const int cl = half * 256 + lane * 8;  // column within the CTA's kCols
+  const int c = blockIdx.x * kCols + cl;
   double acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.0;
@@ -278,8 +286,8 @@ __global__ void __launch_bounds__(kPoolThreads, FFWD_POOL_MINB)
 #pragma unroll
   for (int i = 0; i < 8; ++i) red[quarter][cl + i] = acc[i];
   __syncthreads();
-  for (int j = threadIdx.x; j < kPoolCols; j += kPoolThreads) {
-    const int col = blockIdx.x * kPoolCols + j;
+  for (int j = threadIdx.x; j < kCols; j += kThr) {
+    const int col = blockIdx.x * kCols + j;
     if (col < d) {
       double v = 0.0;
 #pragma unroll
@@ -737,11 +745,20 @@ cudaError_t launch_pool(const void* x, bool x_is_f32, int T, int d, int blk_begi
   cudaError_t e = launch_k(softmax_kernel, dim3(blk_count), dim3(kBlockTokens), 0, s, 1, T,
                            blk_begin, lg, probs);
   if (e != cudaSuccess) return e;
+  const float* pr = probs;
+  if (static_cast<long>(g2.x) * g2.y < FFWD_POOL_NARROW_BELOW) {  // under one wave: 256 columns
+    const dim3 g1((d + 255) / 256, blk_count);
+    if (x_is_f32)
+      return launch_k(pooled_kernel<true, 1>, g1, dim3(128), 0, s, 1, x, T, d, blk_begin,
+                      blk_count, pr, pooled);
+    return launch_k(pooled_kernel<false, 1>, g1, dim3(128), 0, s, 1, x, T, d, blk_begin,
+                    blk_count, pr, pooled);
+  }
   if (x_is_f32)
-    return launch_k(pooled_kernel<true>, g2, dim3(kPoolThreads), 0, s, 1, x, T, d, blk_begin,
-                    blk_count, static_cast<const float*>(probs), pooled);
-  return launch_k(pooled_kernel<false>, g2, dim3(kPoolThreads), 0, s, 1, x, T, d, blk_begin,
-                  blk_count, static_cast<const float*>(probs), pooled);
+    return launch_k(pooled_kernel<true, 2>, g2, dim3(kPoolThreads), 0, s, 1, x, T, d, blk_begin,
+                    blk_count, pr, pooled);
+  return launch_k(pooled_kernel<false, 2>, g2, dim3(kPoolThreads), 0, s, 1, x, T, d, blk_begin,
+                  blk_count, pr, pooled);
 }
 
 cudaError_t launch_pool_generic(const void* x, bool x_is_f32, int T, int d, int rpb,
