@@ -592,8 +592,11 @@ __global__ void __launch_bounds__(GTHREADS)
   constexpr int BP = kCzBN + 8;
   constexpr int WC = kCzBN / (4 / RG);  // columns per warp
   constexpr int NJ = WC / 8;
-  __shared__ __align__(16) float As[2][BM * AP];
-  __shared__ __align__(16) float Bs[2][GBK * BP];
+  // chunk ring: 4 deep for 32-row tiles (a split's K, 4 chunks at the 1B shape, is in
+  // flight at once), 2 deep for 64-row tiles (static shared memory)
+  constexpr int kNB = RG == 1 ? 4 : 2;
+  __shared__ __align__(16) float As[kNB][BM * AP];
+  __shared__ __align__(16) float Bs[kNB][GBK * BP];
   __shared__ __align__(16) double part[BM * kCzBN];
   cg::cluster_group cl = cg::this_cluster();
   const int z = static_cast<int>(cl.block_rank()), nz = static_cast<int>(cl.num_blocks());
@@ -637,18 +640,20 @@ __global__ void __launch_bounds__(GTHREADS)
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  int buf = 0;
-  if (k_lo < k_hi) load_chunk(0, k_lo);
-  for (int k0 = k_lo; k0 < k_hi; k0 += GBK) {
-    if (k0 + GBK < k_hi) {
-      load_chunk(buf ^ 1, k0 + GBK);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+  const int nch = k_hi > k_lo ? (k_hi - k_lo + GBK - 1) / GBK : 0;
+#pragma unroll
+  for (int q = 0; q < kNB - 1; ++q) {  // one commit group per chunk slot, empty past the end
+    if (q < nch) load_chunk(q, k_lo + q * GBK);
+    else cp_async_commit();
+  }
+  for (int ch = 0; ch < nch; ++ch) {
+    const int nx = ch + kNB - 1;
+    if (nx < nch) load_chunk(nx % kNB, k_lo + nx * GBK);
+    else cp_async_commit();
+    cp_async_wait<kNB - 1>();  // chunk ch has landed
     __syncthreads();
-    const float* as = As[buf];
-    const float* bs = Bs[buf];
+    const float* as = As[ch % kNB];
+    const float* bs = Bs[ch % kNB];
 #pragma unroll
     for (int ks = 0; ks < GBK / 4; ++ks) {
       double a[4], bb[NJ];
@@ -663,7 +668,6 @@ __global__ void __launch_bounds__(GTHREADS)
         for (int j = 0; j < NJ; ++j) dmma(acc[i][j], a[i], bb[j]);
     }
     __syncthreads();
-    buf ^= 1;
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i)
