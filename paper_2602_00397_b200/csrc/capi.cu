@@ -168,7 +168,7 @@ int run_predictor(const void* x, bool x_is_f32, int T, int d, int b0, int nb, co
               "pool");
   }
   {
-    StageTimer tm(kW1, s, gemm_f64acc_kernels(nb, d, r, true));
+    StageTimer tm(kW1, s, gemm_f64acc_kernels(nb, d, r, true));  // (the cluster path's count)
     FFWD_CUDA(launch_gemm_f64acc(p.pooled, w1, p.hidden, nb, d, r, true, p.partial, s), "w1");
   }
   {

@@ -850,9 +850,14 @@ cudaError_t launch_gemm_f64acc(const float* A, const float* B, float* C, int M, 
                                bool relu, double* partial, cudaStream_t s) {
   if (M <= 0 || N <= 0) return cudaSuccess;
   if (partial) {
-    if (const int cz = cluster_splits(M, K, N); cz > 1)
-      return M > 32 ? launch_cluster_splitk<2>(A, B, C, M, K, N, relu, cz, s)
-                    : launch_cluster_splitk<1>(A, B, C, M, K, N, relu, cz, s);
+    if (const int cz = cluster_splits(M, K, N); cz > 1) {
+      const cudaError_t e = M > 32 ? launch_cluster_splitk<2>(A, B, C, M, K, N, relu, cz, s)
+                                   : launch_cluster_splitk<1>(A, B, C, M, K, N, relu, cz, s);
+      // a device that cannot co-schedule 16-CTA clusters (e.g. a small MIG slice) rejects
+      // the launch synchronously: take the partials + reduce path below instead
+      if (e != cudaErrorInvalidClusterSize && e != cudaErrorLaunchOutOfResources) return e;
+      (void)cudaGetLastError();
+    }
   }
   const int splits = partial ? gemm_splits(M, K, N) : 1;
   const int kper = ((K + splits - 1) / splits + GBK - 1) / GBK * GBK;
